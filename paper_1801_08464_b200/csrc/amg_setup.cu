@@ -1,0 +1,574 @@
+// AMG setup kernels: row-sign normalisation, strength of connection, PMIS
+// coarsening, extended+i interpolation (optional max_elmts truncation) and
+// L1 row norms.
+//
+// Reference counterparts: strength_graph
+// (amg.py:88-103, same definition), rs_splitting (amg.py:106-158, replaced by
+// PMIS), classical_interpolation (amg.py:206-276, replaced by extended+i),
+// Gauss-Seidel handles (amg.py:279-286, replaced by L1-Jacobi).  The
+// operation order of every floating-point result is the one pinned in
+// oracle/csrc/amg_oracle.c, so C/F splittings, P patterns and P values are
+// bit-identical to the oracle (the file is compiled with --fmad=false and uses
+// explicit __d*_rn intrinsics on the pinned sequences).
+#include "ops.cuh"
+#include "hash.cuh"
+#include "amg_kernels.cuh"
+
+namespace mg {
+
+enum { UNDEC = 0, FPT = 1, CPT = 2 };
+
+// ---- diagonal ----------------------------------------------------------------
+__global__ void k_row_diag(int n, const int *rp, const int *ci, const double *v, double *d) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  int found = -1;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32)
+    if (ci[q] == wid) found = q;
+  unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
+  double val = 0.0;
+  if (bal) {
+    int src = __ffs(bal) - 1;
+    int q = __shfl_sync(0xffffffffu, found, src);
+    val = __dadd_rn(0.0, v[q]);
+  }
+  if (lane == 0) d[wid] = val;
+}
+
+void row_diag(const Csr &a, double *d) {
+  if (!a.nr) return;
+  k_row_diag<<<grid_for((int64_t)a.nr * 32, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, d);
+  check_launch("row_diag");
+}
+
+// ---- row-sign normalisation (amg.py:296-301; diags @ csr drops exact zeros) ----
+__global__ void k_sign_count(int n, const int *rp, const double *v, const double *sgn, int *cnt) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  int c = 0;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) c += __dmul_rn(sgn[wid], v[q]) != 0.0;
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if (lane == 0) cnt[wid] = c;
+}
+__global__ void k_sign_fill(int n, const int *rp, const int *ci, const double *v, const double *sgn,
+                            const int *orp, int *oci, double *ov) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  int o = orp[wid];
+  for (int q0 = rp[wid]; q0 < rp[wid + 1]; q0 += 32) {
+    int q = q0 + lane;
+    double val = q < rp[wid + 1] ? __dmul_rn(sgn[wid], v[q]) : 0.0;
+    bool keep = q < rp[wid + 1] && val != 0.0;
+    unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      int p = o + __popc(bal & ((1u << lane) - 1));
+      oci[p] = ci[q];
+      ov[p] = val;
+    }
+    o += __popc(bal);
+  }
+}
+__global__ void k_sign_of_diag(int n, const double *d, double *sgn, int *flags) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double di = d[i];
+  if (di == 0.0) atomicMin(&flags[0], i);
+  if (di < 0.0) atomicExch(&flags[1], 1);
+  sgn[i] = di < 0.0 ? -1.0 : 1.0;
+}
+
+// returns false when no row needed flipping (out untouched)
+bool sign_normalise(const Csr &a, Csr &out, DBuf<double> &sgn) {
+  int n = a.nr;
+  DBuf<double> d(n);
+  row_diag(a, d.p);
+  sgn.alloc(n);
+  DBuf<int> flags(2);
+  int init[2] = {0x7fffffff, 0};
+  h2d(flags.p, init, sizeof(init));
+  if (n) {
+    k_sign_of_diag<<<grid_for(n, 256), 256, 0, stream()>>>(n, d.p, sgn.p, flags.p);
+    check_launch("sign_of_diag");
+  }
+  int hf[2];
+  d2h(hf, flags.p, sizeof(hf));
+  if (hf[0] != 0x7fffffff) throw MgError(MG_ERR_AMG_SETUP, "AMG expects a nonzero diagonal", hf[0]);
+  if (!hf[1]) { sgn.release(); return false; }
+  out.nr = n;
+  out.nc = a.nc;
+  out.b = 1;
+  out.rp.alloc((size_t)n + 1);
+  DBuf<int> cnt(n);
+  k_sign_count<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.v.p, sgn.p, cnt.p);
+  check_launch("sign_count");
+  out.nnz = exclusive_scan_i32_to_i32(cnt.p, out.rp.p, n);
+  out.ci.alloc((size_t)out.nnz);
+  out.v.alloc((size_t)out.nnz);
+  k_sign_fill<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, a.v.p, sgn.p, out.rp.p,
+                                                                     out.ci.p, out.v.p);
+  check_launch("sign_fill");
+  return true;
+}
+
+// ---- strength of connection (amg.py:88-103) ------------------------------------
+__global__ void k_strength(int n, const int *rp, const int *ci, const double *v, double theta, int8_t *s,
+                           int *any) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  int b = rp[wid], e = rp[wid + 1];
+  bool neg = false;
+  for (int q = b + lane; q < e; q += 32) neg |= (ci[q] != wid) && (v[q] < 0.0);
+  bool has_neg = __any_sync(0xffffffffu, neg);
+  double rmax = 0.0;
+  for (int q = b + lane; q < e; q += 32) {
+    bool off = ci[q] != wid;
+    double a = v[q];
+    double cand = (off && a < 0.0) ? -a : ((off && !has_neg) ? fabs(a) : 0.0);
+    rmax = fmax(rmax, cand);
+  }
+  for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  double thr = __dmul_rn(theta, rmax);
+  int cnt = 0;
+  for (int q = b + lane; q < e; q += 32) {
+    bool off = ci[q] != wid;
+    double a = v[q];
+    double cand = (off && a < 0.0) ? -a : ((off && !has_neg) ? fabs(a) : 0.0);
+    int8_t st = (rmax > 0.0 && cand >= thr) ? 1 : 0;
+    s[q] = st;
+    cnt += st;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(any, cnt);
+}
+
+int64_t strength(const Csr &a, double theta, DBuf<int8_t> &s) {
+  s.alloc((size_t)(a.nnz ? a.nnz : 1));
+  DBuf<int> any(1);
+  dzero(any.p, sizeof(int));
+  if (a.nr) {
+    k_strength<<<grid_for((int64_t)a.nr * 32, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, theta,
+                                                                         s.p, any.p);
+    check_launch("strength");
+  }
+  int h = 0;
+  d2h(&h, any.p, sizeof(int));
+  return h;
+}
+
+// ---- PMIS ---------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_st_count(int n, const int *rp, const int *ci, const int8_t *s, int *cnt) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32)
+    if (s[q] && ci[q] != wid) atomicAdd(&cnt[ci[q]], 1);
+}
+__global__ void k_st_fill(int n, const int *rp, const int *ci, const int8_t *s, int *pos, int *tind) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32)
+    if (s[q] && ci[q] != wid) tind[atomicAdd(&pos[ci[q]], 1)] = wid;
+}
+__global__ void k_pmis_init(int n, const int *trp, uint64_t seed, int level, double *mu, int8_t *state,
+                            int *undecided) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int st = trp[i + 1] - trp[i];
+  uint64_t x = seed ^ ((uint64_t)(uint32_t)level * 0x9E3779B97F4A7C15ULL) ^ (uint64_t)(int64_t)i;
+  double u = __dmul_rn((double)(splitmix64(x) >> 11), 1.0 / 9007199254740992.0);
+  mu[i] = __dadd_rn((double)st, u);
+  state[i] = st == 0 ? FPT : UNDEC;
+  if (st) atomicAdd(undecided, 1);
+}
+__device__ __forceinline__ bool beats(double mi, int i, double mj, int j) {
+  return mi > mj || (mi == mj && i > j);
+}
+__global__ void k_pmis_select(int n, const int *rp, const int *ci, const int8_t *s, const int *trp,
+                              const int *tind, const double *mu, const int8_t *state, int8_t *newc) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int8_t res = 0;
+  if (state[i] == UNDEC) {
+    double mi = mu[i];
+    bool best = true;
+    for (int q = rp[i]; q < rp[i + 1] && best; ++q) {
+      int j = ci[q];
+      if (!s[q] || j == i || state[j] != UNDEC) continue;
+      if (!beats(mi, i, mu[j], j)) best = false;
+    }
+    for (int q = trp[i]; q < trp[i + 1] && best; ++q) {
+      int j = tind[q];
+      if (state[j] != UNDEC) continue;
+      if (!beats(mi, i, mu[j], j)) best = false;
+    }
+    res = best ? 1 : 0;
+  }
+  newc[i] = res;
+}
+__global__ void k_pmis_update(int n, const int *rp, const int *ci, const int8_t *s, const int8_t *newc,
+                              int8_t *state, int *undecided) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (state[i] != UNDEC) return;
+  if (newc[i]) { state[i] = CPT; return; }
+  for (int q = rp[i]; q < rp[i + 1]; ++q) {
+    int k = ci[q];
+    if (s[q] && k != i && (newc[k] || state[k] == CPT)) { state[i] = FPT; return; }
+  }
+  atomicAdd(undecided, 1);
+}
+
+int pmis(const Csr &a, const int8_t *s, uint64_t seed, int level, DBuf<int8_t> &state) {
+  int n = a.nr;
+  state.alloc((size_t)(n ? n : 1));
+  if (!n) return 0;
+  DBuf<int> tcnt((size_t)n + 1), trp((size_t)n + 1), tpos((size_t)n);
+  dzero(tcnt.p, sizeof(int) * ((size_t)n + 1));
+  k_st_count<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, tcnt.p);
+  check_launch("st_count");
+  int64_t nt = exclusive_scan_i32_to_i32(tcnt.p, trp.p, n);
+  DBuf<int> tind((size_t)(nt ? nt : 1));
+  d2d(tpos.p, trp.p, sizeof(int) * (size_t)n);
+  k_st_fill<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, tpos.p, tind.p);
+  check_launch("st_fill");
+  DBuf<double> mu(n);
+  DBuf<int8_t> newc(n);
+  DBuf<int> und(1);
+  dzero(und.p, sizeof(int));
+  k_pmis_init<<<grid_for(n, 256), 256, 0, stream()>>>(n, trp.p, seed, level, mu.p, state.p, und.p);
+  check_launch("pmis_init");
+  int hu = 0;
+  d2h(&hu, und.p, sizeof(int));
+  int rounds = 0;
+  while (hu > 0) {
+    ++rounds;
+    k_pmis_select<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, trp.p, tind.p, mu.p, state.p,
+                                                           newc.p);
+    check_launch("pmis_select");
+    dzero(und.p, sizeof(int));
+    k_pmis_update<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, newc.p, state.p, und.p);
+    check_launch("pmis_update");
+    d2h(&hu, und.p, sizeof(int));
+    if (rounds > 100000) throw MgError(MG_ERR_AMG_SETUP, "PMIS did not terminate");
+  }
+  return rounds;
+}
+
+// ---- extended+i interpolation ----------------------------------------------------
+__device__ __forceinline__ bool opposite(double v, double dkk) {
+  return (v < 0.0 && dkk > 0.0) || (v > 0.0 && dkk < 0.0);
+}
+
+// candidate bound per row: C rows 1; F rows: strong C + sum_{strong F k} |row k|
+__global__ void k_ext_ub(int n, const int *rp, const int *ci, const int8_t *s, const int8_t *state, int *ub) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  int64_t c = 0;
+  if (state[wid] != CPT)
+    for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) {
+      int j = ci[q];
+      if (j == wid || !s[q]) continue;
+      c += state[j] == FPT ? (rp[j + 1] - rp[j]) : 1;
+    }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) ub[wid] = c > 0x3fffffff ? 0x3fffffff : (int)c;
+}
+
+struct ExtArgs {
+  const int *rp, *ci;
+  const double *v;
+  const int8_t *s, *state;
+  const int *cmap;
+  int max_elmts;
+  int mode;
+  int *cnt;
+  const int *prp;
+  int *pci;
+  double *pv;
+  int *bad;
+};
+
+__device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) {
+  const int *rp = A.rp, *ci = A.ci;
+  const double *v = A.v;
+  const int8_t *s = A.s, *state = A.state;
+  if (state[i] == CPT) {
+    if (lane == 0) {
+      if (A.mode == 0) A.cnt[i] = 1;
+      else { A.pci[A.prp[i]] = A.cmap[i]; A.pv[A.prp[i]] = 1.0; }
+    }
+    return;
+  }
+  unsigned mask = (unsigned)T - 1;
+  table_clear(t, T, lane);
+  int b = rp[i], e = rp[i + 1];
+  int mine = 0;
+  for (int q = b + lane; q < e; q += 32) {
+    int j = ci[q];
+    if (j != i && s[q] && state[j] == CPT) mine += hash_insert(t.keys, mask, j);
+  }
+  for (int q = b + lane; q < e; q += 32) {
+    int k = ci[q];
+    if (k == i || !s[q] || state[k] != FPT) continue;
+    for (int q2 = rp[k]; q2 < rp[k + 1]; ++q2) {
+      int l = ci[q2];
+      if (l != k && s[q2] && state[l] == CPT) mine += hash_insert(t.keys, mask, l);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  int u = mine;
+  __syncwarp();
+  int outlen = (A.max_elmts > 0 && u > A.max_elmts) ? A.max_elmts : u;
+  if (A.mode == 0) {
+    if (lane == 0) A.cnt[i] = outlen;
+    return;
+  }
+  if (u == 0) return;
+  table_sort(t, T, u, lane);
+  double *num = t.acc;
+  for (int q = lane; q < u; q += 32) num[q] = 0.0;
+  __syncwarp();
+  // direct numerators a_ij, j in Chat (distinct j: lane parallel)
+  for (int q = b + lane; q < e; q += 32) {
+    int j = ci[q];
+    if (j == i) continue;
+    int sl = hash_find_opt(t.keys, mask, j);
+    if (sl >= 0) { int p = t.pos[sl]; num[p] = __dadd_rn(num[p], v[q]); }
+  }
+  __syncwarp();
+  // dt: a_ii, then weak lumps in row order (sequential in lane 0)
+  double dt = 0.0;
+  if (lane == 0) {
+    for (int q = b; q < e; ++q)
+      if (ci[q] == i) dt = __dadd_rn(dt, v[q]);
+    for (int q = b; q < e; ++q) {
+      int j = ci[q];
+      if (j == i) continue;
+      if (hash_find_opt(t.keys, mask, j) >= 0) continue;
+      if (s[q] && state[j] == FPT) continue;
+      dt = __dadd_rn(dt, v[q]);
+    }
+  }
+  // distribution through strong F neighbours k, in row order
+  for (int q = b; q < e; ++q) {
+    int k = ci[q];
+    if (k == i || !s[q] || state[k] != FPT) continue;
+    double aik = v[q];
+    int kb = rp[k], ke = rp[k + 1];
+    // a_kk (single stored diagonal, 0 when absent)
+    int found = -1;
+    for (int q2 = kb + lane; q2 < ke; q2 += 32)
+      if (ci[q2] == k) found = q2;
+    unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
+    double akk = 0.0;
+    if (bal) akk = __dadd_rn(0.0, v[__shfl_sync(0xffffffffu, found, __ffs(bal) - 1)]);
+    double beta = 0.0;
+    if (lane == 0) {
+      for (int q2 = kb; q2 < ke; ++q2) {
+        int l = ci[q2];
+        if (l == k) continue;
+        double val = v[q2];
+        if (!opposite(val, akk)) continue;
+        if (l == i || hash_find_opt(t.keys, mask, l) >= 0) beta = __dadd_rn(beta, val);
+      }
+    }
+    beta = __shfl_sync(0xffffffffu, beta, 0);
+    if (beta == 0.0) {
+      if (lane == 0) dt = __dadd_rn(dt, aik);
+      continue;
+    }
+    double f = __ddiv_rn(aik, beta);
+    for (int q2 = kb + lane; q2 < ke; q2 += 32) {
+      int l = ci[q2];
+      if (l == k) continue;
+      double val = v[q2];
+      if (!opposite(val, akk)) continue;
+      int sl = hash_find_opt(t.keys, mask, l);
+      if (sl >= 0) { int p = t.pos[sl]; num[p] = __dadd_rn(num[p], __dmul_rn(f, val)); }
+    }
+    if (lane == 0) {
+      for (int q2 = kb; q2 < ke; ++q2)
+        if (ci[q2] == i && opposite(v[q2], akk)) dt = __dadd_rn(dt, __dmul_rn(f, v[q2]));
+    }
+    __syncwarp();
+  }
+  dt = __shfl_sync(0xffffffffu, dt, 0);
+  if (dt == 0.0) {
+    if (lane == 0) atomicMin(A.bad, i);
+    return;
+  }
+  for (int q = lane; q < u; q += 32) num[q] = __ddiv_rn(-num[q], dt);
+  __syncwarp();
+  int o = A.prp[i];
+  if (outlen == u) {
+    for (int q = lane; q < u; q += 32) {
+      A.pci[o + q] = A.cmap[t.list[q]];
+      A.pv[o + q] = num[q];
+    }
+    return;
+  }
+  // truncation: keep the max_elmts largest |w| (ties: smaller column), rescale
+  int *flag = t.pos;  // pos no longer needed
+  for (int q = lane; q < u; q += 32) flag[q] = 0;
+  __syncwarp();
+  for (int r = 0; r < outlen; ++r) {
+    double bw = -1.0;
+    int bq = 0x7fffffff;
+    for (int q = lane; q < u; q += 32) {
+      if (flag[q]) continue;
+      double aw = fabs(num[q]);
+      if (aw > bw || (aw == bw && q < bq)) { bw = aw; bq = q; }
+    }
+    for (int o2 = 16; o2 > 0; o2 >>= 1) {
+      double ow = __shfl_xor_sync(0xffffffffu, bw, o2);
+      int oq = __shfl_xor_sync(0xffffffffu, bq, o2);
+      if (ow > bw || (ow == bw && oq < bq)) { bw = ow; bq = oq; }
+    }
+    if (lane == 0 && bq < u) flag[bq] = 1;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    double s_all = 0.0, s_kept = 0.0;
+    for (int q = 0; q < u; ++q) s_all = __dadd_rn(s_all, num[q]);
+    for (int q = 0; q < u; ++q)
+      if (flag[q]) s_kept = __dadd_rn(s_kept, num[q]);
+    double scale = s_kept != 0.0 ? __ddiv_rn(s_all, s_kept) : 1.0;
+    int w = 0;
+    for (int q = 0; q < u; ++q)
+      if (flag[q]) {
+        A.pci[o + w] = A.cmap[t.list[q]];
+        A.pv[o + w] = __dmul_rn(num[q], scale);
+        ++w;
+      }
+  }
+}
+
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_ext_smem(int nrows, const int *rows, ExtArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpTables t = carve(smem + table_bytes(T) * wid, T);
+  for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB) ext_row(rows[r], T, t, lane, A);
+}
+__global__ void k_ext_gmem(int nrows, const int *rows, const int64_t *goff, const int *gsize,
+                           unsigned char *pool, ExtArgs A) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= nrows) return;
+  int T = gsize[wid];
+  ext_row(rows[wid], T, carve(pool + goff[wid], T), lane, A);
+}
+
+template <int T, int WPB>
+static void launch_ext(int nrows, const int *rows, const ExtArgs &A) {
+  if (!nrows) return;
+  size_t sm = table_bytes(T) * WPB;
+  MG_CUDA(cudaFuncSetAttribute(k_ext_smem<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int grid = (nrows + WPB - 1) / WPB;
+  int cap = g_ctx->num_sms * 16;
+  if (grid > cap) grid = cap;
+  k_ext_smem<T, WPB><<<grid, WPB * 32, sm, stream()>>>(nrows, rows, A);
+  check_launch("ext_interp");
+}
+
+__global__ void k_cflags(int n, const int8_t *state, int *flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = state[i] == CPT;
+}
+__global__ void k_cmap_from_scan(int n, const int8_t *state, const int *scan, int *cmap) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) cmap[i] = state[i] == CPT ? scan[i] : -1;
+}
+
+int coarse_map(const int8_t *state, int n, DBuf<int> &cmap) {
+  DBuf<int> flag((size_t)(n ? n : 1)), scan((size_t)n + 1);
+  cmap.alloc((size_t)(n ? n : 1));
+  if (n) {
+    k_cflags<<<grid_for(n, 256), 256, 0, stream()>>>(n, state, flag.p);
+    check_launch("cflags");
+  }
+  int nc = (int)exclusive_scan_i32_to_i32(flag.p, scan.p, n);
+  if (n) {
+    k_cmap_from_scan<<<grid_for(n, 256), 256, 0, stream()>>>(n, state, scan.p, cmap.p);
+    check_launch("cmap");
+  }
+  return nc;
+}
+
+Csr ext_interp(const Csr &a, const int8_t *s, const int8_t *state, const int *cmap, int nc, int max_elmts) {
+  int n = a.nr;
+  Csr p;
+  p.nr = n;
+  p.nc = nc;
+  p.b = 1;
+  p.rp.alloc((size_t)n + 1);
+  DBuf<int> ub((size_t)(n ? n : 1)), cnt((size_t)(n ? n : 1)), bad(1);
+  int big = 0x7fffffff;
+  h2d(bad.p, &big, sizeof(int));
+  if (n) {
+    k_ext_ub<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, state, ub.p);
+    check_launch("ext_ub");
+  }
+  RowBins bins;
+  bins.build(ub.p, n);
+  ExtArgs A{a.rp.p, a.ci.p, a.v.p, s, state, cmap, max_elmts, 0, cnt.p, nullptr, nullptr, nullptr, bad.p};
+  auto run = [&]() {
+    launch_ext<256, 8>(bins.cnt[0], bins.rows.p + bins.off[0], A);
+    launch_ext<1024, 4>(bins.cnt[1], bins.rows.p + bins.off[1], A);
+    launch_ext<4096, 2>(bins.cnt[2], bins.rows.p + bins.off[2], A);
+    int n3 = bins.cnt[3];
+    if (n3) {
+      k_ext_gmem<<<grid_for((int64_t)n3 * 32, 128), 128, 0, stream()>>>(n3, bins.rows.p + bins.off[3],
+                                                                         bins.goff.p, bins.gsize.p,
+                                                                         bins.pool.p, A);
+      check_launch("ext_gmem");
+    }
+  };
+  run();
+  p.nnz = exclusive_scan_i32_to_i32(cnt.p, p.rp.p, n);
+  p.ci.alloc((size_t)p.nnz);
+  p.v.alloc((size_t)p.nnz);
+  A.mode = 1;
+  A.prp = p.rp.p;
+  A.pci = p.ci.p;
+  A.pv = p.v.p;
+  run();
+  int hb = 0;
+  d2h(&hb, bad.p, sizeof(int));
+  if (hb != big)
+    throw MgError(MG_ERR_AMG_SETUP, "extended interpolation hit a zero pivot at row " + std::to_string(hb), hb);
+  return p;
+}
+
+// ---- L1 row norms: d_i = sum_j |a_ij| (sequential per row), dinv = 1/d --------
+__global__ void k_l1inv(int n, const int *rp, const double *v, double *dinv) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double d = 0.0;
+  for (int q = rp[i]; q < rp[i + 1]; ++q) d = __dadd_rn(d, fabs(v[q]));
+  dinv[i] = __ddiv_rn(1.0, d);
+}
+void l1_inverse(const Csr &a, double *dinv) {
+  if (!a.nr) return;
+  k_l1inv<<<grid_for(a.nr, 128), 128, 0, stream()>>>(a.nr, a.rp.p, a.v.p, dinv);
+  check_launch("l1inv");
+}
+
+// ---- dense copy of a (small) CSR ----------------------------------------------
+__global__ void k_to_dense(int n, int nc, const int *rp, const int *ci, const double *v, double *d) {
+  int i = blockIdx.x;
+  for (int q = rp[i] + threadIdx.x; q < rp[i + 1]; q += blockDim.x) d[(int64_t)i * nc + ci[q]] = v[q];
+}
+void to_dense(const Csr &a, double *d) {
+  dzero(d, sizeof(double) * (size_t)a.nr * a.nc);
+  if (!a.nr) return;
+  k_to_dense<<<a.nr, 64, 0, stream()>>>(a.nr, a.nc, a.rp.p, a.ci.p, a.v.p, d);
+  check_launch("to_dense");
+}
+
+}  // namespace mg

@@ -1,0 +1,182 @@
+// Per-cell block kernels: batched b x b inverses of the diagonal blocks held
+// in registers, block scaling Ahat = D^-1 A (scalar CSR, cell-major), and the
+// per-apply prescale z = D^-1 v.
+//
+// Reference counterpart: _BlockDiagSolver (mgr.py:212-242; np.linalg.inv per
+// cell, batched einsum apply).  The pinned operation order (closed-form
+// adjugate, k-ascending products, no FMA) is the one restated in
+// oracle/blockscale.py, so Dinv and Ahat are bit-identical to the oracle
+// (SURVEY.md §7 D2/D3).  HBM-bound: read 8 b^2 N (diagonal blocks) + write
+// 8 b^2 N; scaling reads/writes every block once.
+#include "ops.cuh"
+#include "blockscale.cuh"
+
+namespace mg {
+
+template <int B>
+__device__ __forceinline__ bool invert_block(const double *a, double *inv) {
+  if (B == 2) {
+    double det = __dsub_rn(__dmul_rn(a[0], a[3]), __dmul_rn(a[1], a[2]));
+    if (det == 0.0) return false;
+    inv[0] = __ddiv_rn(a[3], det);
+    inv[1] = __ddiv_rn(-a[1], det);
+    inv[2] = __ddiv_rn(-a[2], det);
+    inv[3] = __ddiv_rn(a[0], det);
+    return true;
+  } else {
+#define G(i, j) a[(i) * 3 + (j)]
+    double c00 = __dsub_rn(__dmul_rn(G(1, 1), G(2, 2)), __dmul_rn(G(1, 2), G(2, 1)));
+    double c01 = __dsub_rn(__dmul_rn(G(1, 2), G(2, 0)), __dmul_rn(G(1, 0), G(2, 2)));
+    double c02 = __dsub_rn(__dmul_rn(G(1, 0), G(2, 1)), __dmul_rn(G(1, 1), G(2, 0)));
+    double det = __dadd_rn(__dadd_rn(__dmul_rn(G(0, 0), c00), __dmul_rn(G(0, 1), c01)), __dmul_rn(G(0, 2), c02));
+    if (det == 0.0) return false;
+    inv[0 * 3 + 0] = __ddiv_rn(c00, det);
+    inv[1 * 3 + 0] = __ddiv_rn(c01, det);
+    inv[2 * 3 + 0] = __ddiv_rn(c02, det);
+    inv[0 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(G(0, 2), G(2, 1)), __dmul_rn(G(0, 1), G(2, 2))), det);
+    inv[1 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(G(0, 0), G(2, 2)), __dmul_rn(G(0, 2), G(2, 0))), det);
+    inv[2 * 3 + 1] = __ddiv_rn(__dsub_rn(__dmul_rn(G(0, 1), G(2, 0)), __dmul_rn(G(0, 0), G(2, 1))), det);
+    inv[0 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(G(0, 1), G(1, 2)), __dmul_rn(G(0, 2), G(1, 1))), det);
+    inv[1 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(G(0, 2), G(1, 0)), __dmul_rn(G(0, 0), G(1, 2))), det);
+    inv[2 * 3 + 2] = __ddiv_rn(__dsub_rn(__dmul_rn(G(0, 0), G(1, 1)), __dmul_rn(G(0, 1), G(1, 0))), det);
+#undef G
+    return true;
+  }
+}
+
+template <int B>
+__global__ void k_block_inv(int N, const int *rp, const int *ci, const double *v, double *dinv,
+                            int *diag_pos, int *bad) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int dp = -1;
+  for (int q = rp[i]; q < rp[i + 1]; ++q)
+    if (ci[q] == i) { dp = q; break; }
+  diag_pos[i] = dp;
+  double a[B * B], inv[B * B];
+  if (dp < 0) { atomicMin(bad, i); return; }
+#pragma unroll
+  for (int t = 0; t < B * B; ++t) a[t] = v[(int64_t)dp * B * B + t];
+  if (!invert_block<B>(a, inv)) { atomicMin(bad, i); return; }
+#pragma unroll
+  for (int t = 0; t < B * B; ++t) dinv[(int64_t)i * B * B + t] = inv[t];
+}
+
+// scaled entry (r, c) of block q in block row i: sum_k Dinv_i[r][k] * A_q[k][c]
+template <int B>
+__device__ __forceinline__ double scaled(const double *d, const double *a, int r, int c) {
+  double s = __dmul_rn(d[r * B + 0], a[0 * B + c]);
+#pragma unroll
+  for (int k = 1; k < B; ++k) s = __dadd_rn(s, __dmul_rn(d[r * B + k], a[k * B + c]));
+  return s;
+}
+
+// one thread per scalar row (cell i, var r): mode 0 count, mode 1 fill
+template <int B>
+__global__ void k_scale_rows(int N, const int *rp, const int *ci, const double *v, const double *dinv,
+                             int mode, int *cnt, const int *orp, int *oci, double *ov) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)N * B) return;
+  int i = (int)(t / B), r = (int)(t % B);
+  double d[B * B];
+#pragma unroll
+  for (int q = 0; q < B * B; ++q) d[q] = dinv[(int64_t)i * B * B + q];
+  int c0 = 0;
+  int o = mode ? orp[t] : 0;
+  for (int q = rp[i]; q < rp[i + 1]; ++q) {
+    int j = ci[q];
+    if (j == i) {
+      if (mode) { oci[o + c0] = i * B + r; ov[o + c0] = 1.0; }
+      ++c0;
+      continue;
+    }
+    const double *a = v + (int64_t)q * B * B;
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      double s = scaled<B>(d, a, r, c);
+      if (s != 0.0) {
+        if (mode) { oci[o + c0] = j * B + c; ov[o + c0] = s; }
+        ++c0;
+      }
+    }
+  }
+  if (!mode) cnt[t] = c0;
+}
+
+template <int B>
+__global__ void k_block_apply(int N, const double *__restrict__ dinv, const double *__restrict__ x,
+                              double *__restrict__ z) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double d[B * B], xv[B];
+#pragma unroll
+  for (int q = 0; q < B * B; ++q) d[q] = dinv[(int64_t)i * B * B + q];
+#pragma unroll
+  for (int q = 0; q < B; ++q) xv[q] = x[(int64_t)i * B + q];
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+    double s = __dmul_rn(d[r * B + 0], xv[0]);
+#pragma unroll
+    for (int k = 1; k < B; ++k) s = __dadd_rn(s, __dmul_rn(d[r * B + k], xv[k]));
+    z[(int64_t)i * B + r] = s;
+  }
+}
+
+__global__ void k_diag_pattern(int N, int *rp, int *ci) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) { rp[i] = i; ci[i] = i; }
+  if (i == N) rp[N] = N;
+}
+
+void block_scale(const Csr &a, Csr &dinv, Csr &ahat) {
+  const int B = a.b;
+  if (B != 2 && B != 3) throw MgError(MG_ERR_UNSUPPORTED, "block_scale: b must be 2 or 3");
+  if (a.nr != a.nc) throw MgError(MG_ERR_DIM_MISMATCH, "block_scale: square block matrix required");
+  int N = a.nr;
+  dinv.alloc(N, N, N, B);
+  k_diag_pattern<<<grid_for((int64_t)N + 1, 256), 256, 0, stream()>>>(N, dinv.rp.p, dinv.ci.p);
+  check_launch("diag_pattern");
+  DBuf<int> dpos(N), bad(1);
+  int big = 0x7fffffff;
+  h2d(bad.p, &big, sizeof(int));
+  if (B == 2)
+    k_block_inv<2><<<grid_for(N, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, dpos.p, bad.p);
+  else
+    k_block_inv<3><<<grid_for(N, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, dpos.p, bad.p);
+  check_launch("block_inv");
+  int hb = 0;
+  d2h(&hb, bad.p, sizeof(int));
+  if (hb != big) throw MgError(MG_ERR_SINGULAR, "singular (or missing) diagonal block at cell " + std::to_string(hb), hb);
+  int64_t n = (int64_t)N * B;
+  DBuf<int> cnt((size_t)n);
+  ahat.nr = ahat.nc = (int)n;
+  ahat.b = 1;
+  ahat.rp.alloc((size_t)n + 1);
+  if (B == 2)
+    k_scale_rows<2><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 0, cnt.p, nullptr, nullptr, nullptr);
+  else
+    k_scale_rows<3><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 0, cnt.p, nullptr, nullptr, nullptr);
+  check_launch("scale_count");
+  ahat.nnz = exclusive_scan_i32_to_i32(cnt.p, ahat.rp.p, (int)n);
+  ahat.ci.alloc((size_t)ahat.nnz);
+  ahat.v.alloc((size_t)ahat.nnz);
+  if (B == 2)
+    k_scale_rows<2><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 1, nullptr, ahat.rp.p, ahat.ci.p, ahat.v.p);
+  else
+    k_scale_rows<3><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 1, nullptr, ahat.rp.p, ahat.ci.p, ahat.v.p);
+  check_launch("scale_fill");
+}
+
+void block_apply(const Csr &dinv, const double *x, double *z) {
+  int N = dinv.nr;
+  if (!N) return;
+  if (dinv.b == 2)
+    k_block_apply<2><<<grid_for(N, 256), 256, 0, stream()>>>(N, dinv.v.p, x, z);
+  else if (dinv.b == 3)
+    k_block_apply<3><<<grid_for(N, 256), 256, 0, stream()>>>(N, dinv.v.p, x, z);
+  else
+    throw MgError(MG_ERR_UNSUPPORTED, "block_apply: b must be 2 or 3");
+  check_launch("block_apply");
+}
+
+}  // namespace mg

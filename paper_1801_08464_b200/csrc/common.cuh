@@ -1,0 +1,137 @@
+// Shared infrastructure for libmgrgpu: context, errors, device buffers, CSR.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+#include <stdexcept>
+#include <cstring>
+#include "../../include/mgrgpu.h"
+
+namespace mg {
+
+struct MgError {
+  int code;
+  std::string msg;
+  int64_t row;
+  MgError(int c, std::string m, int64_t r = -1) : code(c), msg(std::move(m)), row(r) {}
+};
+
+#define MG_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t _e = (call);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      throw ::mg::MgError(MG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+struct Ctx;
+extern thread_local Ctx *g_ctx;  // context of the current API call
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t err_row = -1;
+  int64_t launches = 0;
+  int64_t dev_bytes = 0;
+  int num_sms = 148;
+  int profiling = 0;
+  mg_timing timing{};
+  // scratch
+  double *red = nullptr;        // reduction partials (device)
+  size_t red_cap = 0;
+  double *hbuf = nullptr;       // pinned host scratch
+  size_t hbuf_cap = 0;
+  void *cub_tmp = nullptr;
+  size_t cub_cap = 0;
+  int *dflag = nullptr;         // device int scratch (4 ints)
+  int *hflag = nullptr;         // pinned mirror
+};
+
+inline cudaStream_t stream() { return g_ctx->stream; }
+inline void count_launch(int n = 1) { g_ctx->launches += n; }
+inline void check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw MgError(MG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  g_ctx->launches++;
+}
+
+void *dmalloc(size_t bytes);
+void dfree(void *p, size_t bytes);
+void *cub_scratch(size_t bytes);
+double *red_scratch(size_t n);
+double *host_scratch(size_t n);
+void sync();
+
+// RAII device buffer (stream-ordered allocation on the context stream)
+template <typename T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t n_) { alloc(n_); }
+  void alloc(size_t n_) {
+    release();
+    n = n_;
+    p = n ? (T *)dmalloc(n * sizeof(T)) : nullptr;
+  }
+  void release() {
+    if (p) dfree(p, n * sizeof(T));
+    p = nullptr;
+    n = 0;
+  }
+  T *detach() { T *q = p; p = nullptr; n = 0; return q; }
+  ~DBuf() { if (p && g_ctx) release(); }
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf &operator=(DBuf &&o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  T *get() const { return p; }
+};
+
+// Device CSR; b > 1 means block CSR with b*b row-major values per entry.
+struct Csr {
+  int nr = 0, nc = 0, b = 1;
+  int64_t nnz = 0;
+  DBuf<int> rp, ci;
+  DBuf<double> v;
+  Csr() = default;
+  Csr(Csr &&) = default;
+  Csr &operator=(Csr &&) = default;
+  void alloc(int nr_, int nc_, int64_t nnz_, int b_ = 1) {
+    nr = nr_; nc = nc_; nnz = nnz_; b = b_;
+    rp.alloc((size_t)nr + 1);
+    ci.alloc((size_t)nnz);
+    v.alloc((size_t)nnz * b * b);
+  }
+  double bytes_spmv() const {  // algorithmic bytes of y = A x
+    double vb = (double)nnz * (8.0 * b * b + 4.0) + 4.0 * (nr + 1);
+    return vb + 8.0 * b * nc + 8.0 * b * nr;
+  }
+};
+
+inline int grid_for(int64_t work, int block, int max_blocks = 0) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (max_blocks && g > max_blocks) g = max_blocks;
+  if (g > 2147483647LL) g = 2147483647LL;
+  return (int)g;
+}
+
+// host <-> device helpers (synchronous on the ctx stream)
+void h2d(void *dst, const void *src, size_t bytes);
+void d2h(void *dst, const void *src, size_t bytes);
+void dzero(void *dst, size_t bytes);
+void d2d(void *dst, const void *src, size_t bytes);
+
+// scans / reductions (CUB)
+// out[0]=0, out[i+1] = sum in[0..i]; returns total (host)
+int64_t exclusive_scan_i32_to_i32(const int *in, int *out, int n);
+int64_t exclusive_scan_i32_to_i64(const int *in, int64_t *out, int n);
+int64_t reduce_sum_i32(const int *in, int n);
+int64_t count_u8(const uint8_t *in, int n);
+
+}  // namespace mg

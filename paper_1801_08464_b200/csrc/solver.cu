@@ -1,0 +1,602 @@
+// Solver drivers: AMG hierarchy (amg.py:289-386 structure with PMIS /
+// extended+i / L1-Jacobi), MGR hierarchy (mgr.py:265-377) and restarted
+// right-preconditioned GMRES (krylov.py:44-144).  All vectors stay on the
+// device; the host only runs the <= (m+1) x m Hessenberg / Givens recurrence.
+#include <cmath>
+#include <algorithm>
+#include "ops.cuh"
+#include "solver.cuh"
+#include "sparse_util.cuh"
+#include "amg_kernels.cuh"
+#include "blockscale.cuh"
+
+namespace mg {
+
+static const int DENSE_LIMIT = 8192;
+
+// ---- profiling of hot kernels ---------------------------------------------------
+static thread_local std::vector<ProfScope *> *g_open = nullptr;
+struct ProfRec { int kind; cudaEvent_t a, b; };
+static thread_local std::vector<ProfRec> g_prof;
+
+ProfScope::ProfScope(int k) : kind(k) {
+  if (!g_ctx->profiling) return;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, stream());
+}
+ProfScope::~ProfScope() {
+  if (!a) return;
+  cudaEventRecord(b, stream());
+  g_prof.push_back({kind, a, b});
+}
+void prof_reset() {
+  for (auto &r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  g_prof.clear();
+  g_ctx->timing.spmv_ms = g_ctx->timing.vcycle_ms = 0;
+  g_ctx->timing.spmv_calls = g_ctx->timing.vcycle_calls = 0;
+}
+void prof_collect() {
+  if (g_prof.empty()) return;
+  cudaStreamSynchronize(stream());
+  for (auto &r : g_prof) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (r.kind == 0) { g_ctx->timing.spmv_ms += ms; g_ctx->timing.spmv_calls++; }
+    else { g_ctx->timing.vcycle_ms += ms; g_ctx->timing.vcycle_calls++; }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+}
+
+// ================================ AMG ==============================================
+double Amg::cycle_bytes() const {
+  // sum_l (pre+post) (SpMV_l + 24 n_l) + SpMV_l + SpMV(R_l) + SpMV(P_l) + 16 n_l
+  double tot = 0;
+  for (size_t l = 0; l + 1 < L.size(); ++l) {
+    const AmgLevel &v = L[l];
+    double spmv = v.A.bytes_spmv();
+    double sweeps = opts.pre + opts.post;
+    tot += sweeps * (spmv + 24.0 * v.n) + spmv + 8.0 * v.n + v.R.bytes_spmv() + v.P.bytes_spmv() + 16.0 * v.n;
+  }
+  tot += 8.0 * (double)cn * cn;
+  return tot;
+}
+
+std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "amg_setup: scalar CSR required");
+  if (a.nr != a.nc) throw MgError(MG_ERR_AMG_SETUP, "AMG expects a square operator");
+  auto h = std::make_unique<Amg>();
+  h->opts = o;
+  {
+    AmgLevel l0;
+    Csr flipped;
+    DBuf<double> sgn;
+    if (sign_normalise(a, flipped, sgn)) {
+      l0.A = std::move(flipped);
+      h->sign = std::move(sgn);
+      h->has_sign = true;
+    } else {
+      l0.A = copy_csr(a);
+    }
+    l0.n = a.nr;
+    h->L.push_back(std::move(l0));
+  }
+  while (h->L.back().n > o.cutoff && (int)h->L.size() < o.max_levels) {
+    int li = (int)h->L.size() - 1;
+    AmgLevel &cur = h->L[li];
+    DBuf<int8_t> s;
+    if (strength(cur.A, o.theta, s) == 0) break;  // no strong connection: no progress
+    DBuf<int8_t> state;
+    pmis(cur.A, s.p, o.seed, li, state);
+    DBuf<int> cmap;
+    int nc = coarse_map(state.p, cur.n, cmap);
+    if (nc == 0) throw MgError(MG_ERR_AMG_SETUP, "coarsening produced an empty C set");
+    if (nc == cur.n) break;
+    Csr p = ext_interp(cur.A, s.p, state.p, cmap.p, nc, o.max_elmts);
+    Csr r = transpose(p);
+    Csr ap = spgemm(cur.A, p);
+    Csr ac = spgemm(r, ap);
+    cur.P = std::move(p);
+    cur.R = std::move(r);
+    cur.split = std::move(state);
+    AmgLevel nxt;
+    nxt.n = ac.nr;
+    nxt.A = std::move(ac);
+    h->L.push_back(std::move(nxt));
+  }
+  for (size_t l = 0; l < h->L.size(); ++l) {
+    AmgLevel &v = h->L[l];
+    size_t n = (size_t)(v.n ? v.n : 1);
+    v.x.alloc(n);
+    v.b.alloc(n);
+    v.r.alloc(n);
+    v.t.alloc(n);
+    if (l + 1 < h->L.size()) {
+      v.l1inv.alloc(n);
+      l1_inverse(v.A, v.l1inv.p);
+    }
+  }
+  AmgLevel &last = h->L.back();
+  if (last.n > std::max(o.cutoff, 200) && last.n > DENSE_LIMIT)
+    throw MgError(MG_ERR_AMG_SETUP, "coarsening stalled at n=" + std::to_string(last.n) +
+                                        " (dense coarsest solve limited to " + std::to_string(DENSE_LIMIT) + ")");
+  h->cn = last.n;
+  if (h->cn) {
+    DBuf<double> dense((size_t)h->cn * h->cn);
+    to_dense(last.A, dense.p);
+    h->cinv.alloc((size_t)h->cn * h->cn);
+    int bad = dense_inverse(dense.p, h->cinv.p, h->cn);
+    if (bad >= 0) throw MgError(MG_ERR_SINGULAR, "coarsest AMG operator is singular", bad);
+  }
+  return h;
+}
+
+static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero) {
+  AmgLevel &v = h.L[l];
+  if (l + 1 == (int)h.L.size()) {
+    dense_matvec(h.cinv.p, b, x, h.cn);
+    return;
+  }
+  AmgLevel &nx = h.L[l + 1];
+  double *cur = x, *oth = v.t.p;
+  for (int s = 0; s < h.opts.pre; ++s) {
+    if (x_zero) {
+      vmul(cur, v.l1inv.p, b, v.n);
+      x_zero = false;
+    } else {
+      jacobi_sweep(v.A, cur, b, v.l1inv.p, oth);
+      std::swap(cur, oth);
+    }
+  }
+  const double *res = b;
+  if (!x_zero) {
+    residual(v.A, cur, b, v.r.p);
+    res = v.r.p;
+  }
+  spmv(v.R, res, nx.b.p);
+  vcycle(h, l + 1, nx.b.p, nx.x.p, true);
+  if (x_zero) spmv(v.P, nx.x.p, cur);
+  else spmv_add(v.P, nx.x.p, cur);
+  for (int s = 0; s < h.opts.post; ++s) {
+    jacobi_sweep(v.A, cur, b, v.l1inv.p, oth);
+    std::swap(cur, oth);
+  }
+  if (cur != x) vcopy(x, cur, v.n);
+}
+
+void amg_vcycle(Amg &h, const double *b, const double *x0, double *x) {
+  AmgLevel &l0 = h.L[0];
+  const double *bb = b;
+  if (h.has_sign) {
+    vmul(l0.b.p, h.sign.p, b, l0.n);
+    bb = l0.b.p;
+  }
+  if (x0) {
+    if (x0 != x) vcopy(x, x0, l0.n);
+    vcycle(h, 0, bb, x, false);
+  } else {
+    vcycle(h, 0, bb, x, true);
+  }
+}
+
+void amg_apply(Amg &h, const double *b, double *x) {
+  ProfScope ps(1);
+  amg_vcycle(h, b, nullptr, x);
+  for (int c = 1; c < h.opts.cycles; ++c) amg_vcycle(h, b, x, x);
+}
+
+// ================================ MGR ==============================================
+static void fsolver_setup(FSolver &fs, Csr &aff, const LevelSpec &sp, const AmgOpts &ao) {
+  fs.kind = sp.frelax;
+  fs.sweeps = sp.sweeps;
+  fs.nf = aff.nr;
+  size_t nf = (size_t)(aff.nr ? aff.nr : 1);
+  fs.t1.alloc(nf);
+  fs.t2.alloc(nf);
+  if (sp.frelax == FR_JACOBI) {
+    DBuf<double> d(nf);
+    row_diag(aff, d.p);
+    std::vector<double> hd(aff.nr);
+    d2h(hd.data(), d.p, sizeof(double) * aff.nr);
+    for (int i = 0; i < aff.nr; ++i)
+      if (hd[i] == 0.0) throw MgError(MG_ERR_ZERO_F_DIAG, "zero diagonal in A_ff at fine row " + std::to_string(i), i);
+    for (auto &v : hd) v = 1.0 / v;
+    fs.invd.alloc(nf);
+    h2d(fs.invd.p, hd.data(), sizeof(double) * aff.nr);
+  } else if (sp.frelax == FR_AMG) {
+    AmgOpts o = ao;
+    o.max_levels = sp.max_levels ? sp.max_levels : ao.max_levels;
+    o.pre = sp.pre;
+    o.post = sp.post;
+    o.cycles = 1;
+    fs.amg = amg_setup(aff, o);
+  } else if (sp.frelax == FR_EXACT) {
+    if (aff.nr > DENSE_LIMIT)
+      throw MgError(MG_ERR_UNSUPPORTED, "FRelax('exact') on the GPU is limited to n_f <= 8192");
+    DBuf<double> dense((size_t)aff.nr * aff.nr);
+    to_dense(aff, dense.p);
+    fs.dinv.alloc((size_t)aff.nr * aff.nr);
+    int bad = dense_inverse(dense.p, fs.dinv.p, aff.nr);
+    if (bad >= 0) throw MgError(MG_ERR_SINGULAR, "A_ff is singular", bad);
+  } else {
+    throw MgError(MG_ERR_UNSUPPORTED, "FRelax('gauss_seidel') is not available on the GPU path");
+  }
+}
+
+static void fsolve(FSolver &fs, const Csr &aff, const double *r, double *x) {
+  if (fs.kind == FR_JACOBI) {
+    vmul(x, fs.invd.p, r, fs.nf);
+    double *cur = x, *oth = fs.t1.p;
+    for (int s = 1; s < fs.sweeps; ++s) {
+      jacobi_sweep(aff, cur, r, fs.invd.p, oth);
+      std::swap(cur, oth);
+    }
+    if (cur != x) vcopy(x, cur, fs.nf);
+  } else if (fs.kind == FR_AMG) {
+    amg_vcycle(*fs.amg, r, nullptr, x);
+  } else {
+    dense_matvec(fs.dinv.p, r, x, fs.nf);
+  }
+}
+
+// per-cell block-diagonal relaxation (uniform block size)
+__global__ void k_bd_apply(int nblk, int k, const int *idx, const double *inv, const double *r, double *x) {
+  int bi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= nblk) return;
+  const int *id = idx + (int64_t)bi * k;
+  const double *m = inv + (int64_t)bi * k * k;
+  for (int a = 0; a < k; ++a) {
+    double s = 0.0;
+    for (int c = 0; c < k; ++c) s += m[a * k + c] * r[id[c]];
+    x[id[a]] = s;
+  }
+}
+__global__ void k_bd_gather(int nblk, int k, const int *idx, const int *rp, const int *ci, const double *v,
+                            double *blk) {
+  int bi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= nblk) return;
+  const int *id = idx + (int64_t)bi * k;
+  for (int a = 0; a < k; ++a)
+    for (int c = 0; c < k; ++c) {
+      double val = 0.0;
+      int row = id[a], col = id[c];
+      for (int q = rp[row]; q < rp[row + 1]; ++q)
+        if (ci[q] == col) { val = v[q]; break; }
+      blk[((int64_t)bi * k + a) * k + c] = val;
+    }
+}
+// small dense inverses by Gauss-Jordan with partial pivoting, one thread per block (k <= 8)
+__global__ void k_bd_invert(int nblk, int k, double *blk, double *inv, int *bad) {
+  int bi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= nblk) return;
+  double a[8][16];
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < 2 * k; ++j) a[i][j] = j < k ? blk[((int64_t)bi * k + i) * k + j] : (j - k == i ? 1.0 : 0.0);
+  for (int c = 0; c < k; ++c) {
+    int p = c;
+    for (int i = c + 1; i < k; ++i)
+      if (fabs(a[i][c]) > fabs(a[p][c])) p = i;
+    if (a[p][c] == 0.0) { atomicMin(bad, bi); return; }
+    if (p != c)
+      for (int j = 0; j < 2 * k; ++j) { double t = a[c][j]; a[c][j] = a[p][j]; a[p][j] = t; }
+    double pv = a[c][c];
+    for (int j = 0; j < 2 * k; ++j) a[c][j] /= pv;
+    for (int i = 0; i < k; ++i) {
+      if (i == c) continue;
+      double f = a[i][c];
+      if (f != 0.0)
+        for (int j = 0; j < 2 * k; ++j) a[i][j] -= f * a[c][j];
+    }
+  }
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) inv[((int64_t)bi * k + i) * k + j] = a[i][k + j];
+}
+
+static std::unique_ptr<BlockDiag> blockdiag_setup(const Csr &a, const std::vector<int64_t> &cells) {
+  // group unknowns by owning cell (stable), all groups must share one size
+  int n = a.nr;
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cells[x] < cells[y]; });
+  std::vector<int> idx;
+  int k = -1, nblk = 0;
+  for (int s = 0; s < n;) {
+    int e = s;
+    while (e < n && cells[order[e]] == cells[order[s]]) ++e;
+    std::vector<int> g(order.begin() + s, order.begin() + e);
+    std::sort(g.begin(), g.end());
+    if (k < 0) k = (int)g.size();
+    if ((int)g.size() != k) throw MgError(MG_ERR_UNSUPPORTED, "global_relax: mixed per-cell block sizes");
+    idx.insert(idx.end(), g.begin(), g.end());
+    ++nblk;
+    s = e;
+  }
+  if (k > 8) throw MgError(MG_ERR_UNSUPPORTED, "global_relax: per-cell blocks larger than 8");
+  auto bd = std::make_unique<BlockDiag>();
+  bd->nblk = nblk;
+  bd->k = k;
+  bd->idx.alloc(idx.size());
+  h2d(bd->idx.p, idx.data(), sizeof(int) * idx.size());
+  DBuf<double> blk((size_t)nblk * k * k);
+  bd->inv.alloc((size_t)nblk * k * k);
+  k_bd_gather<<<grid_for(nblk, 128), 128, 0, stream()>>>(nblk, k, bd->idx.p, a.rp.p, a.ci.p, a.v.p, blk.p);
+  check_launch("bd_gather");
+  DBuf<int> bad(1);
+  int big = 0x7fffffff;
+  h2d(bad.p, &big, sizeof(int));
+  k_bd_invert<<<grid_for(nblk, 64), 64, 0, stream()>>>(nblk, k, blk.p, bd->inv.p, bad.p);
+  check_launch("bd_invert");
+  int hb;
+  d2h(&hb, bad.p, sizeof(int));
+  if (hb != big) throw MgError(MG_ERR_SINGULAR, "singular per-cell block", hb);
+  return bd;
+}
+
+std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan, const AmgOpts &ao,
+                               int coarse_kind, bool post_smoothing, const int64_t *cells_host) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "mgr_setup: scalar CSR required");
+  if (a.nr != a.nc) throw MgError(MG_ERR_DIM_MISMATCH, "mgr_setup: square matrix required");
+  if (coarse_kind != 0 && coarse_kind != 1) throw MgError(MG_ERR_BAD_OPTION, "unknown coarse solver");
+  auto h = std::make_unique<Mgr>();
+  h->n0 = a.nr;
+  h->post_smoothing = post_smoothing;
+  h->coarse_kind = coarse_kind;
+  Csr cur = copy_csr(a);
+  std::vector<int64_t> cells(a.nr);
+  for (int i = 0; i < a.nr; ++i) cells[i] = cells_host ? cells_host[i] : i;
+  for (const LevelSpec &sp : plan) {
+    int n = cur.nr;
+    if ((int)sp.fmask.size() != n) throw MgError(MG_ERR_DIM_MISMATCH, "level plan mask length mismatch");
+    int nf_h = 0;
+    for (uint8_t m : sp.fmask) nf_h += m != 0;
+    if (nf_h == 0 || nf_h == n) continue;
+    MgrLevel lv;
+    lv.n = n;
+    lv.rp = sp.rp;
+    DBuf<uint8_t> mask(n);
+    h2d(mask.p, sp.fmask.data(), n);
+    DBuf<int> fmap, cmap;
+    fc_split(mask.p, n, lv.flist, lv.clist, fmap, cmap, lv.nf, lv.nc);
+    build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
+    Csr ap = spgemm(cur, lv.P);
+    Csr ac = spgemm(lv.R, ap);
+    lv.Aff = extract(cur, lv.flist.p, lv.nf, fmap.p, lv.nf);
+    fsolver_setup(lv.fs, lv.Aff, sp, ao);
+    if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
+    std::vector<int64_t> nxt_cells;
+    {
+      std::vector<int> cl(lv.nc);
+      d2h(cl.data(), lv.clist.p, sizeof(int) * lv.nc);
+      nxt_cells.resize(lv.nc);
+      for (int c = 0; c < lv.nc; ++c) nxt_cells[c] = cells[cl[c]];
+    }
+    cells.swap(nxt_cells);
+    lv.res.alloc(n);
+    lv.rF.alloc(lv.nf);
+    lv.eF.alloc(lv.nf);
+    lv.rc.alloc(lv.nc);
+    lv.ec.alloc(lv.nc);
+    lv.A = std::move(cur);
+    cur = std::move(ac);
+    h->L.push_back(std::move(lv));
+  }
+  if (coarse_kind == 0) {
+    h->camg = amg_setup(cur, ao);
+  } else {
+    if (cur.nr > DENSE_LIMIT) throw MgError(MG_ERR_UNSUPPORTED, "coarse='exact' on the GPU is limited to n <= 8192");
+    h->cn = cur.nr;
+    DBuf<double> dense((size_t)cur.nr * cur.nr);
+    to_dense(cur, dense.p);
+    h->cinv.alloc((size_t)cur.nr * cur.nr);
+    int bad = dense_inverse(dense.p, h->cinv.p, cur.nr);
+    if (bad >= 0) throw MgError(MG_ERR_SINGULAR, "coarse operator is singular", bad);
+  }
+  h->coarse_A = std::move(cur);
+  return h;
+}
+
+static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
+  if (k == h.L.size()) {
+    if (h.coarse_kind == 0) amg_apply(*h.camg, r, e);
+    else dense_matvec(h.cinv.p, r, e, h.cn);
+    return;
+  }
+  MgrLevel &lv = h.L[k];
+  bool zero = true;
+  if (lv.bd) {
+    k_bd_apply<<<grid_for(lv.bd->nblk, 128), 128, 0, stream()>>>(lv.bd->nblk, lv.bd->k, lv.bd->idx.p,
+                                                                 lv.bd->inv.p, r, e);
+    check_launch("bd_apply");
+    zero = false;
+  }
+  auto resid = [&]() -> const double * {
+    if (zero) return r;
+    residual(lv.A, e, r, lv.res.p);
+    return lv.res.p;
+  };
+  auto f_relax = [&]() {
+    const double *rr = resid();
+    gather(lv.rF.p, rr, lv.flist.p, lv.nf);
+    fsolve(lv.fs, lv.Aff, lv.rF.p, lv.eF.p);
+    if (zero) {
+      vfill(e, 0.0, lv.n);
+      scatter_set(e, lv.eF.p, lv.flist.p, lv.nf);
+    } else {
+      scatter_add(e, lv.eF.p, lv.flist.p, lv.nf);
+    }
+    zero = false;
+  };
+  auto coarse_correct = [&]() {
+    const double *rr = resid();
+    spmv(lv.R, rr, lv.rc.p);
+    apply_level(h, k + 1, lv.rc.p, lv.ec.p);
+    if (zero) spmv(lv.P, lv.ec.p, e);
+    else spmv_add(lv.P, lv.ec.p, e);
+    zero = false;
+  };
+  if (h.post_smoothing) {
+    coarse_correct();
+    f_relax();
+  } else {
+    f_relax();
+    coarse_correct();
+  }
+}
+
+void mgr_apply(Mgr &h, const double *r, double *e) {
+  const double *rr = r;
+  if (h.has_prescale) {
+    block_apply(h.prescale, r, h.pre_buf.p);
+    rr = h.pre_buf.p;
+  }
+  apply_level(h, 0, rr, e);
+}
+
+// ================================ GMRES ============================================
+static void op_apply(const Csr &a, const double *x, double *y) {
+  ProfScope ps(0);
+  spmv(a, x, y);
+}
+
+GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts &o, double a_norm) {
+  int64_t n = (int64_t)a.nr * a.b;
+  if ((int64_t)a.nc * a.b != n) throw MgError(MG_ERR_DIM_MISMATCH, "gmres: square operator required");
+  if (m && m->n0 != n) throw MgError(MG_ERR_DIM_MISMATCH, "gmres: preconditioner dimension mismatch");
+  if (o.rel_tol <= 0.0) throw MgError(MG_ERR_BAD_OPTION, "rel_tol must be positive");
+  if (o.restart < 1 || o.max_iter < 1) throw MgError(MG_ERR_BAD_OPTION, "restart and max_iter must be at least 1");
+  GmresOut out;
+  bool use_anorm = a_norm >= 0.0;
+  double b_norm = nrm2(b, n);
+  out.rhs_norm = b_norm;
+  if (b_norm == 0.0) {
+    vfill(x, 0.0, n);
+    out.converged = 1;
+    return out;
+  }
+  double tol = o.rel_tol * b_norm;
+  auto accepted = [&](double res, double xn) {
+    if (res <= tol) return true;
+    return use_anorm && res <= o.rel_tol * (a_norm * xn + b_norm);
+  };
+  int mmax = std::min(o.restart, o.max_iter);
+  DBuf<double> V((size_t)(mmax + 1) * n), w(n), z(n), r(n), xt(n), u(n), t(n), proj((size_t)2 * (mmax + 1) + 8);
+  double *c_dev = proj.p, *c2_dev = proj.p + (mmax + 1), *nrm_dev = proj.p + 2 * (mmax + 1);
+  std::vector<double> hbuf(2 * (mmax + 1) + 1);
+  vfill(x, 0.0, n);
+  int total = 0;
+  auto precond = [&](const double *v, double *out_) -> const double * {
+    if (!m) return v;
+    mgr_apply(*m, v, out_);
+    return out_;
+  };
+  while (true) {
+    double res;
+    if (total) {
+      op_apply(a, x, t.p);
+      vsub(r.p, b, t.p, n);
+      res = nrm2(r.p, n);
+    } else {
+      vcopy(r.p, b, n);
+      res = b_norm;
+    }
+    double xn = use_anorm ? nrm2(x, n) : 0.0;
+    if (accepted(res, xn)) {
+      out.iterations = total;
+      out.converged = 1;
+      out.residual_norm = res;
+      return out;
+    }
+    if (total >= o.max_iter) {
+      out.iterations = total;
+      out.converged = 0;
+      out.residual_norm = res;
+      return out;
+    }
+    int mm = std::min(o.restart, o.max_iter - total);
+    std::vector<double> H((size_t)(mm + 1) * mm, 0.0), cs(mm, 0.0), sn(mm, 0.0), g(mm + 1, 0.0);
+    auto h_at = [&](int i, int j) -> double & { return H[(size_t)i * mm + j]; };
+    vdiv_scalar(V.p, r.p, res, n);
+    g[0] = res;
+    auto assemble = [&](int k, double *xout) {
+      std::vector<double> y(k, 0.0);
+      for (int i = k - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int j = i + 1; j < k; ++j) s -= h_at(i, j) * y[j];
+        y[i] = s / h_at(i, i);
+      }
+      if (k) {
+        h2d(c_dev, y.data(), sizeof(double) * k);
+        combine(V.p, n, k, c_dev, u.p, n);
+      } else {
+        vfill(u.p, 0.0, n);
+      }
+      const double *mz = precond(u.p, z.p);
+      if (xout != x) vcopy(xout, x, n);
+      vadd(xout, mz, n);
+    };
+    int k = 0;
+    bool early = false;
+    double early_res = 0.0;
+    for (int j = 0; j < mm; ++j) {
+      double *vj = V.p + (int64_t)j * n;
+      const double *mz = precond(vj, z.p);
+      op_apply(a, mz, w.p);
+      int K = j + 1;
+      mdot(V.p, n, K, w.p, n, c_dev);
+      if (o.reorth) {
+        update_mdot(V.p, n, K, c_dev, w.p, n, c2_dev);
+        update_norm2(V.p, n, K, c2_dev, w.p, n, nrm_dev);
+      } else {
+        update_norm2(V.p, n, K, c_dev, w.p, n, nrm_dev);
+      }
+      d2h(hbuf.data(), proj.p, sizeof(double) * (2 * (mmax + 1) + 1));
+      for (int i = 0; i < K; ++i) h_at(i, j) = o.reorth ? hbuf[i] + hbuf[(mmax + 1) + i] : hbuf[i];
+      double hn = std::sqrt(hbuf[2 * (mmax + 1)]);
+      h_at(j + 1, j) = hn;
+      ++total;
+      k = j + 1;
+      for (int i = 0; i < j; ++i) {
+        double t = cs[i] * h_at(i, j) + sn[i] * h_at(i + 1, j);
+        h_at(i + 1, j) = -sn[i] * h_at(i, j) + cs[i] * h_at(i + 1, j);
+        h_at(i, j) = t;
+      }
+      double den = std::hypot(h_at(j, j), h_at(j + 1, j));
+      if (den == 0.0) {
+        k = j;
+        break;
+      }
+      cs[j] = h_at(j, j) / den;
+      sn[j] = h_at(j + 1, j) / den;
+      h_at(j, j) = den;
+      h_at(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      bool happy = hn <= 1e-14 * std::max(res, 1.0);
+      if (std::fabs(g[j + 1]) <= tol || happy || total >= o.max_iter) break;
+      if (use_anorm && o.check_every && k % o.check_every == 0) {
+        assemble(k, xt.p);
+        op_apply(a, xt.p, t.p);
+        vsub(r.p, b, t.p, n);
+        double rt = nrm2(r.p, n);
+        if (accepted(rt, nrm2(xt.p, n))) {
+          early = true;
+          early_res = rt;
+          break;
+        }
+      }
+      vdiv_scalar(V.p + (int64_t)(j + 1) * n, w.p, hn, n);
+    }
+    if (early) {
+      vcopy(x, xt.p, n);
+      out.iterations = total;
+      out.converged = 1;
+      out.residual_norm = early_res;
+      return out;
+    }
+    assemble(k, x);
+  }
+}
+
+}  // namespace mg

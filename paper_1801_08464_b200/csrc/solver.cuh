@@ -1,0 +1,115 @@
+// Solver objects: AMG hierarchy, MGR hierarchy, GMRES driver.
+#pragma once
+#include <memory>
+#include <vector>
+#include "common.cuh"
+
+namespace mg {
+
+struct AmgOpts {
+  double theta = 0.25;
+  int max_levels = 25, cutoff = 50, pre = 1, post = 1, cycles = 1, max_elmts = 4;
+  uint64_t seed = 0;
+};
+
+struct AmgLevel {
+  Csr A;                  // level operator (level 0: row-sign-normalised copy)
+  Csr P, R;               // interpolation from level l+1, R = P^T
+  DBuf<int8_t> split;     // C/F marker of this level (0/1/2)
+  DBuf<double> l1inv;     // 1 / sum_j |a_ij|
+  DBuf<double> x, b, r, t;
+  int n = 0;
+};
+
+struct Amg {
+  AmgOpts opts;
+  std::vector<AmgLevel> L;
+  DBuf<double> sign;
+  bool has_sign = false;
+  DBuf<double> cinv;      // dense inverse of the coarsest operator
+  int cn = 0;
+  double cycle_bytes() const;
+};
+
+std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o);
+void amg_vcycle(Amg &h, const double *b, const double *x0, double *x);
+void amg_apply(Amg &h, const double *b, double *x);
+
+enum { RP_INJECTIVE = 0, RP_NONINJECTIVE = 1, RP_INJECTION = 2, RP_IDEAL = 3 };
+enum { FR_JACOBI = 0, FR_GS = 1, FR_AMG = 2, FR_EXACT = 3 };
+
+struct LevelSpec {
+  std::vector<uint8_t> fmask;
+  int rp = RP_INJECTIVE, frelax = FR_JACOBI, sweeps = 1, pre = 1, post = 1, max_levels = 0;
+  int global_relax = 0;
+};
+
+struct FSolver {
+  int kind = FR_JACOBI, sweeps = 1;
+  DBuf<double> invd;           // jacobi
+  std::unique_ptr<Amg> amg;    // amg
+  DBuf<double> dinv;           // exact (dense inverse)
+  DBuf<double> t1, t2;
+  int nf = 0;
+};
+
+struct BlockDiag {             // per-cell block-diagonal relaxation (mgr.py:212-242)
+  int nblk = 0, k = 0;         // uniform block size k
+  DBuf<int> idx;               // nblk * k unknowns
+  DBuf<double> inv;            // nblk * k * k
+};
+
+struct MgrLevel {
+  Csr A, R, P, Aff;
+  int n = 0, nf = 0, nc = 0, rp = 0;
+  DBuf<int> flist, clist;
+  FSolver fs;
+  std::unique_ptr<BlockDiag> bd;
+  DBuf<double> res, rF, eF, rc, ec;
+};
+
+struct Mgr {
+  std::vector<MgrLevel> L;
+  int coarse_kind = 0;
+  std::unique_ptr<Amg> camg;
+  DBuf<double> cinv;
+  int cn = 0;
+  Csr coarse_A;
+  bool post_smoothing = false;
+  int n0 = 0;
+  Csr prescale;                // optional per-cell D^-1 (block diagonal)
+  bool has_prescale = false;
+  DBuf<double> pre_buf;
+};
+
+std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan, const AmgOpts &ao,
+                               int coarse_kind, bool post_smoothing, const int64_t *cells_host);
+void mgr_apply(Mgr &h, const double *r, double *e);
+
+struct GmresOpts {
+  double rel_tol = 1e-12;
+  int max_iter = 400, restart = 30, reorth = 1, check_every = 25;
+};
+struct GmresOut {
+  int iterations = 0, converged = 0;
+  double residual_norm = 0, rhs_norm = 0;
+};
+GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts &o, double a_norm);
+
+// build_rp (mgr_ops.cu)
+void fc_split(const uint8_t *fmask_dev, int n, DBuf<int> &flist, DBuf<int> &clist, DBuf<int> &fmap,
+              DBuf<int> &cmap, int &nf, int &nc);
+void build_rp(const Csr &a, const int *fmap, const int *cmap, const int *flist, const int *clist, int nf,
+              int nc, int kind, Csr &r, Csr &p);
+
+// profiling of the hot kernels inside a solve
+struct ProfScope {
+  int kind;  // 0 spmv, 1 vcycle
+  cudaEvent_t a = nullptr, b = nullptr;
+  explicit ProfScope(int k);
+  ~ProfScope();
+};
+void prof_reset();
+void prof_collect();
+
+}  // namespace mg

@@ -1,0 +1,14 @@
+// Sparse-sparse host launchers (spgemm.cu).
+#pragma once
+#include "common.cuh"
+
+namespace mg {
+// C = A B, scipy csr_matmat semantics (exact zeros dropped, sorted columns)
+Csr spgemm(const Csr &a, const Csr &b);
+// A^T with ascending columns per row
+Csr transpose(const Csr &a);
+// rows_dev: nr source rows (sorted); cmap_dev: column map (source col -> new col or -1)
+Csr extract(const Csr &a, const int *rows_dev, int nr, const int *cmap_dev, int nc);
+Csr copy_csr(const Csr &a);
+void scale_i64(int64_t *a, int64_t s, int n);
+}  // namespace mg

@@ -1,0 +1,373 @@
+// Sparse-sparse kernels: SpGEMM with scipy csr_matmat semantics, transpose,
+// submatrix extraction.
+//
+// SpGEMM (replaces scipy csr_matmat at triple_product, sparse.py:199-203 —
+// MGR RAP mgr.py:288 and AMG Galerkin amg.py:318):
+// Gustavson row-by-row, one warp per output row, shared-memory hash tables
+// sized by the row's product upper bound (bins of 256 / 1024 / 4096 slots, a
+// global-memory table beyond).  Bit-exact with scipy:
+// each output column accumulates 0 + a_ij1*b_j1k + a_ij2*b_j2k + ... with j
+// in the left row's stored (ascending) order, a separate multiply and add
+// (libmgrgpu is built with --fmad=false), exact zeros dropped, columns sorted.
+// The lanes of the warp split the entries of B_j (distinct columns, so no
+// two lanes touch one accumulator) and step through j in order.
+#include "ops.cuh"
+#include "sparse_util.cuh"
+#include "hash.cuh"
+#include <cub/cub.cuh>
+
+namespace mg {
+
+// One output row.  mode 0: count unique columns -> cnt[row].
+// mode 1: fill sorted (col, val) at out + base, nonzero count -> nz[row].
+static __device__ void spgemm_row(int row, int T, WarpTables t, int lane, const int *__restrict__ arp,
+                                  const int *__restrict__ aci, const double *__restrict__ av,
+                                  const int *__restrict__ brp, const int *__restrict__ bci,
+                                  const double *__restrict__ bv, int mode, int *cnt,
+                                  const int64_t *base, int *oci, double *ov, int *nz) {
+  unsigned mask = (unsigned)T - 1;
+  table_clear(t, T, lane);
+  int s = arp[row], e = arp[row + 1];
+  int mine = 0;
+  for (int q = s + lane; q < e; q += 32) {
+    int j = aci[q];
+    for (int r = brp[j]; r < brp[j + 1]; ++r) mine += hash_insert(t.keys, mask, bci[r]);
+  }
+  for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+  int u = mine;
+  __syncwarp();
+  if (mode == 0) {
+    if (lane == 0) cnt[row] = u;
+    return;
+  }
+  table_sort(t, T, u, lane);
+  for (int q = lane; q < u; q += 32) t.acc[q] = 0.0;
+  __syncwarp();
+  // ordered accumulation: j ascending (left row order), lanes over B_j
+  for (int q = s; q < e; ++q) {
+    int j = aci[q];
+    double a = av[q];
+    for (int r = brp[j] + lane; r < brp[j + 1]; r += 32) {
+      int p = t.pos[hash_find(t.keys, mask, bci[r])];
+      t.acc[p] = __dadd_rn(t.acc[p], __dmul_rn(a, bv[r]));
+    }
+    __syncwarp();
+  }
+  int64_t o = base[row];
+  int nzc = 0;
+  for (int q = lane; q < u; q += 32) {
+    oci[o + q] = t.list[q];
+    double val = t.acc[q];
+    ov[o + q] = val;
+    nzc += val != 0.0;
+  }
+  for (int off = 16; off > 0; off >>= 1) nzc += __shfl_xor_sync(0xffffffffu, nzc, off);
+  if (lane == 0) nz[row] = nzc;
+}
+
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_spgemm_smem(int nrows, const int *rows, const int *arp,
+                                                          const int *aci, const double *av,
+                                                          const int *brp, const int *bci,
+                                                          const double *bv, int mode, int *cnt,
+                                                          const int64_t *base, int *oci, double *ov,
+                                                          int *nz) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpTables t = carve(smem + table_bytes(T) * wid, T);
+  for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB)
+    spgemm_row(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, mode, cnt, base, oci, ov, nz);
+}
+
+// global-memory tables for rows with huge product bounds (one warp per row)
+__global__ void k_spgemm_gmem(int nrows, const int *rows, const int64_t *tab_off, const int *tab_size,
+                              unsigned char *pool, const int *arp, const int *aci, const double *av,
+                              const int *brp, const int *bci, const double *bv, int mode, int *cnt,
+                              const int64_t *base, int *oci, double *ov, int *nz) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= nrows) return;
+  int T = tab_size[wid];
+  WarpTables t = carve(pool + tab_off[wid], T);
+  spgemm_row(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, mode, cnt, base, oci, ov, nz);
+}
+
+// compaction: drop exact zeros, keep order (warp per row)
+__global__ void k_compact(int m, const int64_t *tmp_rp, const int *tci, const double *tv, const int *rp,
+                          int *ci, double *v) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= m) return;
+  int64_t s = tmp_rp[wid], e = tmp_rp[wid + 1];
+  int o = rp[wid];
+  for (int64_t q0 = s; q0 < e; q0 += 32) {
+    int64_t q = q0 + lane;
+    double val = q < e ? tv[q] : 0.0;
+    bool keep = q < e && val != 0.0;
+    unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      int p = o + __popc(bal & ((1u << lane) - 1));
+      ci[p] = tci[q];
+      v[p] = val;
+    }
+    o += __popc(bal);
+  }
+}
+
+// per-row product upper bound
+__global__ void k_row_ub(int m, const int *arp, const int *aci, const int *brp, int *ub) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= m) return;
+  int64_t s = 0;
+  for (int q = arp[wid] + lane; q < arp[wid + 1]; q += 32) {
+    int j = aci[q];
+    s += brp[j + 1] - brp[j];
+  }
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) ub[wid] = s > 0x3fffffff ? 0x3fffffff : (int)s;
+}
+
+__device__ __forceinline__ int bin_of(int v) { return v <= 128 ? 0 : v <= 512 ? 1 : v <= 2048 ? 2 : 3; }
+
+__global__ void k_bin_count(int m, const int *ub, int *bin_cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) atomicAdd(&bin_cnt[bin_of(ub[i])], 1);
+}
+__global__ void k_bin_fill(int m, const int *ub, int *fillpos, int *rows) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int b = bin_of(ub[i]);
+  int p = atomicAdd(&fillpos[b], 1);
+  rows[p] = i;
+}
+__global__ void k_gmem_tabs(int nr, const int *rows, const int *ub, int *tsz, int *units) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nr) return;
+  int u = ub[rows[i]];
+  int T = 64;
+  while (T < 2 * u) T <<= 1;
+  tsz[i] = T;
+  units[i] = (int)(((int64_t)T * 14 + 15) / 16);  // 16-byte units
+}
+
+__global__ void k_scale_i64(int64_t *a, int64_t s, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] *= s;
+}
+void scale_i64(int64_t *a, int64_t s, int n) {
+  k_scale_i64<<<grid_for(n, 256), 256, 0, stream()>>>(a, s, n);
+  check_launch("scale_i64");
+}
+
+void RowBins::build(const int *ub_dev, int m) {
+  DBuf<int> bc(4);
+  dzero(bc.p, sizeof(int) * 4);
+  if (m) {
+    k_bin_count<<<grid_for(m, 256), 256, 0, stream()>>>(m, ub_dev, bc.p);
+    check_launch("bin_count");
+  }
+  d2h(cnt, bc.p, sizeof(int) * 4);
+  off[0] = 0;
+  for (int b = 1; b < 4; ++b) off[b] = off[b - 1] + cnt[b - 1];
+  h2d(bc.p, off, sizeof(int) * 4);
+  rows.alloc((size_t)(m ? m : 1));
+  if (m) {
+    k_bin_fill<<<grid_for(m, 256), 256, 0, stream()>>>(m, ub_dev, bc.p, rows.p);
+    check_launch("bin_fill");
+  }
+  int n3 = cnt[3];
+  if (n3) {
+    gsize.alloc(n3);
+    DBuf<int> units(n3);
+    goff.alloc((size_t)n3 + 1);
+    k_gmem_tabs<<<grid_for(n3, 256), 256, 0, stream()>>>(n3, rows.p + off[3], ub_dev, gsize.p, units.p);
+    check_launch("gmem_tabs");
+    int64_t tot = exclusive_scan_i32_to_i64(units.p, goff.p, n3);
+    pool.alloc((size_t)tot * 16);
+    scale_i64(goff.p, 16, n3 + 1);
+  }
+}
+
+template <int T, int WPB>
+static void launch_bin(int nrows, const int *rows, const Csr &a, const Csr &b, int mode, int *cnt,
+                       const int64_t *base, int *oci, double *ov, int *nz) {
+  if (!nrows) return;
+  size_t sm = table_bytes(T) * WPB;
+  MG_CUDA(cudaFuncSetAttribute(k_spgemm_smem<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int grid = (nrows + WPB - 1) / WPB;
+  int cap = g_ctx->num_sms * 16;
+  if (grid > cap) grid = cap;
+  k_spgemm_smem<T, WPB><<<grid, WPB * 32, sm, stream()>>>(nrows, rows, a.rp.p, a.ci.p, a.v.p, b.rp.p,
+                                                          b.ci.p, b.v.p, mode, cnt, base, oci, ov, nz);
+  check_launch("spgemm_smem");
+}
+
+Csr spgemm(const Csr &a, const Csr &b) {
+  if (a.b != 1 || b.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spgemm: scalar CSR only");
+  if (a.nc != b.nr) throw MgError(MG_ERR_DIM_MISMATCH, "matmul: inner dimensions differ");
+  int m = a.nr;
+  Csr c;
+  if (m == 0 || a.nnz == 0 || b.nnz == 0) {
+    c.alloc(m, b.nc, 0);
+    dzero(c.rp.p, sizeof(int) * ((size_t)m + 1));
+    return c;
+  }
+  DBuf<int> ub(m), cnt(m), nz(m);
+  k_row_ub<<<grid_for((int64_t)m * 32, 256), 256, 0, stream()>>>(m, a.rp.p, a.ci.p, b.rp.p, ub.p);
+  check_launch("row_ub");
+  RowBins bins;
+  bins.build(ub.p, m);
+  auto run = [&](int mode, const int64_t *base, int *oci, double *ov) {
+    launch_bin<256, 8>(bins.cnt[0], bins.rows.p + bins.off[0], a, b, mode, cnt.p, base, oci, ov, nz.p);
+    launch_bin<1024, 4>(bins.cnt[1], bins.rows.p + bins.off[1], a, b, mode, cnt.p, base, oci, ov, nz.p);
+    launch_bin<4096, 2>(bins.cnt[2], bins.rows.p + bins.off[2], a, b, mode, cnt.p, base, oci, ov, nz.p);
+    int n3 = bins.cnt[3];
+    if (n3) {
+      k_spgemm_gmem<<<grid_for((int64_t)n3 * 32, 128), 128, 0, stream()>>>(
+          n3, bins.rows.p + bins.off[3], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, a.v.p,
+          b.rp.p, b.ci.p, b.v.p, mode, cnt.p, base, oci, ov, nz.p);
+      check_launch("spgemm_gmem");
+    }
+  };
+  run(0, nullptr, nullptr, nullptr);
+  DBuf<int64_t> trp((size_t)m + 1);
+  int64_t total = exclusive_scan_i32_to_i64(cnt.p, trp.p, m);
+  DBuf<int> tci((size_t)total);
+  DBuf<double> tv((size_t)total);
+  run(1, trp.p, tci.p, tv.p);
+  c.nr = m;
+  c.nc = b.nc;
+  c.b = 1;
+  c.rp.alloc((size_t)m + 1);
+  int64_t kept = exclusive_scan_i32_to_i32(nz.p, c.rp.p, m);
+  c.nnz = kept;
+  if (kept == total) {
+    c.ci = std::move(tci);
+    c.v = std::move(tv);
+  } else {
+    c.ci.alloc((size_t)kept);
+    c.v.alloc((size_t)kept);
+    k_compact<<<grid_for((int64_t)m * 32, 256), 256, 0, stream()>>>(m, trp.p, tci.p, tv.p, c.rp.p, c.ci.p,
+                                                                     c.v.p);
+    check_launch("compact");
+  }
+  return c;
+}
+
+// ---- transpose (stable: rows of A^T have ascending columns) -----------------
+__global__ void k_row_ids(int m, const int *rp, int *rid) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= m) return;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) rid[q] = wid;
+}
+__global__ void k_iota(int *a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (int)i;
+}
+__global__ void k_col_count(int64_t nnz, const int *ci, int *cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[ci[i]], 1);
+}
+__global__ void k_permute_entries(int64_t nnz, const int *perm, const int *rid, const double *v, int *tci,
+                                  double *tv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+    int p = perm[i];
+    tci[i] = rid[p];
+    tv[i] = v[p];
+  }
+}
+
+Csr transpose(const Csr &a) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "transpose: scalar CSR only");
+  Csr t;
+  int64_t nnz = a.nnz;
+  t.alloc(a.nc, a.nr, nnz);
+  DBuf<int> cnt((size_t)a.nc + 1);
+  dzero(cnt.p, sizeof(int) * ((size_t)a.nc + 1));
+  if (nnz) {
+    k_col_count<<<grid_for(nnz, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(nnz, a.ci.p, cnt.p);
+    check_launch("col_count");
+  }
+  exclusive_scan_i32_to_i32(cnt.p, t.rp.p, a.nc);
+  if (!nnz) return t;
+  DBuf<int> rid((size_t)nnz), idx((size_t)nnz), keys_out((size_t)nnz), perm((size_t)nnz);
+  k_row_ids<<<grid_for((int64_t)a.nr * 32, 256), 256, 0, stream()>>>(a.nr, a.rp.p, rid.p);
+  check_launch("row_ids");
+  k_iota<<<grid_for(nnz, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(idx.p, nnz);
+  check_launch("iota");
+  int bits = 1;
+  while ((1LL << bits) < (int64_t)a.nc) ++bits;
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, a.ci.p, keys_out.p, idx.p, perm.p, (int)nnz, 0, bits,
+                                  stream());
+  void *tmp = cub_scratch(bytes);
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, a.ci.p, keys_out.p, idx.p, perm.p, (int)nnz, 0, bits,
+                                          stream()));
+  count_launch(4);
+  k_permute_entries<<<grid_for(nnz, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(nnz, perm.p, rid.p,
+                                                                                   a.v.p, t.ci.p, t.v.p);
+  check_launch("permute_entries");
+  return t;
+}
+
+// ---- extract A[rows][:, cols] (keeps stored zeros) ---------------------------
+__global__ void k_extract_count(int nr, const int *rows, const int *rp, const int *ci, const int *cmap,
+                                int *cnt) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= nr) return;
+  int r = rows[wid];
+  int c = 0;
+  for (int q = rp[r] + lane; q < rp[r + 1]; q += 32) c += cmap[ci[q]] >= 0;
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if (lane == 0) cnt[wid] = c;
+}
+__global__ void k_extract_fill(int nr, const int *rows, const int *rp, const int *ci, const double *v,
+                               const int *cmap, const int *orp, int *oci, double *ov) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= nr) return;
+  int r = rows[wid];
+  int o = orp[wid];
+  for (int q0 = rp[r]; q0 < rp[r + 1]; q0 += 32) {
+    int q = q0 + lane;
+    int m = q < rp[r + 1] ? cmap[ci[q]] : -1;
+    unsigned bal = __ballot_sync(0xffffffffu, m >= 0);
+    if (m >= 0) {
+      int p = o + __popc(bal & ((1u << lane) - 1));
+      oci[p] = m;
+      ov[p] = v[q];
+    }
+    o += __popc(bal);
+  }
+}
+
+Csr extract(const Csr &a, const int *rows_dev, int nr, const int *cmap_dev, int nc) {
+  Csr o;
+  o.nr = nr;
+  o.nc = nc;
+  o.rp.alloc((size_t)nr + 1);
+  DBuf<int> cnt((size_t)nr + 1);
+  if (nr) {
+    k_extract_count<<<grid_for((int64_t)nr * 32, 256), 256, 0, stream()>>>(nr, rows_dev, a.rp.p, a.ci.p,
+                                                                            cmap_dev, cnt.p);
+    check_launch("extract_count");
+  }
+  o.nnz = exclusive_scan_i32_to_i32(cnt.p, o.rp.p, nr);
+  o.ci.alloc((size_t)o.nnz);
+  o.v.alloc((size_t)o.nnz);
+  if (nr && o.nnz) {
+    k_extract_fill<<<grid_for((int64_t)nr * 32, 256), 256, 0, stream()>>>(nr, rows_dev, a.rp.p, a.ci.p,
+                                                                           a.v.p, cmap_dev, o.rp.p, o.ci.p,
+                                                                           o.v.p);
+    check_launch("extract_fill");
+  }
+  return o;
+}
+
+Csr copy_csr(const Csr &a) {
+  Csr o;
+  o.alloc(a.nr, a.nc, a.nnz, a.b);
+  d2d(o.rp.p, a.rp.p, sizeof(int) * ((size_t)a.nr + 1));
+  d2d(o.ci.p, a.ci.p, sizeof(int) * (size_t)a.nnz);
+  d2d(o.v.p, a.v.p, sizeof(double) * (size_t)a.nnz * a.b * a.b);
+  return o;
+}
+
+}  // namespace mg

@@ -1,0 +1,108 @@
+"""End-to-end MGR-GMRES on the synthetic block systems (BASELINE.json configs).
+
+The recommended reading of SURVEY.md §8(d) / §7 D2 expressed in the
+reference API, all on the GPU:
+
+    Dinv, Ahat = block_scale(A)                      # per-cell inverses (D3)
+    h = setup_from_matrix(Ahat, plan, amg_opts)      # MGR on Ahat = D^-1 A
+    h.set_prescale(Dinv)                             # M^-1 v = MGR_Ahat(D^-1 v)
+    gmres(A, h, b, GmresOptions(rel_tol, restart=30))
+
+plan: b=2 [(S, NONINJECTIVE, AMG-F)]; b=3 [(S, INJECTIVE, AMG-F), (rho, INJECTIVE,
+AMG-F)], F indices in the cell-major unknown order.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .amg import AmgOptions
+from .krylov import GmresOptions, GmresResult
+from .mgr import FRelax, MgrHierarchy, MgrLevelSpec, RpKind, setup_from_matrix
+from .sparse import DeviceMatrix, block_scale
+
+# defaults used by bench.py, smoke() and the parity tests (oracle uses the same)
+DEFAULT_AMG = dict(strength_theta=0.25, pre_sweeps=2, post_sweeps=2, max_elmts=4)
+DEFAULT_FRELAX = dict(pre=2, post=2)
+
+
+def default_amg_options(**kw) -> AmgOptions:
+    d = dict(DEFAULT_AMG)
+    d.update(kw)
+    return AmgOptions(**d)
+
+
+def default_plan(b: int, n_cells: int, rp=None, frelax: FRelax | None = None):
+    from .synth import mgr_f_indices
+    if rp is None:
+        rp = RpKind.NONINJECTIVE if b == 2 else RpKind.INJECTIVE
+    fr = frelax or FRelax("amg", **DEFAULT_FRELAX)
+    return [(f, MgrLevelSpec((), rp, fr)) for f in mgr_f_indices(b, n_cells, order="cell")]
+
+
+@dataclass
+class SolveStats:
+    setup_ms: float = 0.0
+    solve_ms: float = 0.0
+    iterations: int = 0
+    converged: bool = False
+    relres: float = float("nan")
+    extra: dict = field(default_factory=dict)
+
+
+class SyntheticSolver:
+    """Upload once, then setup / solve on the device."""
+
+    def __init__(self, rel_tol=1e-8, restart=30, max_iter=400, amg_opts=None, rp=None, frelax=None, ctx=None):
+        self.ctx = ctx or _lib.ctx()
+        self.gopts = GmresOptions(rel_tol=rel_tol, restart=restart, max_iter=max_iter)
+        self.amg_opts = amg_opts or default_amg_options()
+        self.rp = rp
+        self.frelax = frelax
+        self.a: DeviceMatrix | None = None
+        self.hier: MgrHierarchy | None = None
+        self.dinv = None
+        self.ahat = None
+
+    def upload(self, sysm) -> DeviceMatrix:
+        self.sysm_meta = (sysm.b, sysm.n_cells)
+        self.a = DeviceMatrix.from_bsr(sysm.rowptr, sysm.col, sysm.vals, ctx=self.ctx)
+        return self.a
+
+    def setup(self, a: DeviceMatrix | None = None, b: int | None = None, n_cells: int | None = None):
+        a = a or self.a
+        b = b or self.sysm_meta[0]
+        n_cells = n_cells or self.sysm_meta[1]
+        if self.hier is not None:
+            self.hier.free()
+            self.hier = None
+        for m in (self.dinv, self.ahat):
+            if m is not None:
+                m.free()
+        self.dinv, self.ahat = block_scale(a)
+        plan = default_plan(b, n_cells, self.rp, self.frelax)
+        self.hier = setup_from_matrix(self.ahat, plan, self.amg_opts)
+        self.hier.set_prescale(self.dinv)
+        # Ahat is copied into the hierarchy; release the standalone copy
+        self.ahat.free()
+        self.ahat = None
+        return self.hier
+
+    def solve(self, rhs) -> GmresResult:
+        from .krylov import gmres
+        return gmres(self.a, self.hier, rhs, self.gopts)
+
+    def solve_system(self, sysm) -> tuple[GmresResult, SolveStats]:
+        t0 = time.perf_counter()
+        self.upload(sysm)
+        self.setup()
+        t1 = time.perf_counter()
+        res = self.solve(sysm.rhs)
+        t2 = time.perf_counter()
+        st = SolveStats(setup_ms=(t1 - t0) * 1e3, solve_ms=(t2 - t1) * 1e3, iterations=res.iterations,
+                        converged=res.converged,
+                        relres=res.residual_norm / res.rhs_norm if res.rhs_norm else 0.0)
+        return res, st

@@ -1,0 +1,142 @@
+"""GPU parity: sparse kernels, block scaling, build_rp (through the C-ABI).
+
+Mirrors the reference's sparse/MGR unit tests (tests/test_sparse.py:27-116,
+tests/test_mgr.py:50-98) with the oracle as the checker; integer outputs and
+the scipy-order products are compared bit for bit.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from helpers import assert_bitwise, assert_close_csr, poisson2d, rand_csr, relerr
+from oracle import blockscale as obs
+from oracle import mgr as omgr
+from paper_1801_08464_b200 import mgr as gmgr
+from paper_1801_08464_b200 import sparse as gsp
+from paper_1801_08464_b200 import synth
+from paper_1801_08464_b200.errors import DimensionMismatch, ZeroFDiagonal
+
+pytestmark = pytest.mark.gpu
+
+
+def test_spmv_identity_and_zero(gpu):
+    n = 17
+    x = np.arange(n, dtype=float)
+    np.testing.assert_array_equal(gsp.spmv(sp.identity(n, format="csr"), x), x)
+    np.testing.assert_array_equal(gsp.spmv(sp.csr_matrix((n, n)), x), np.zeros(n))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_spmv_matches_scipy(gpu, seed):
+    rng = np.random.default_rng(seed)
+    for n, m, dens in ((50, 50, 0.2), (300, 200, 0.05), (2000, 2000, 0.03), (5000, 5000, 0.0005)):
+        a = rand_csr(rng, n, m, dens)
+        x = rng.standard_normal(m)
+        assert relerr(gsp.spmv(a, x), a @ x) <= 1e-14
+
+
+def test_spmv_dimension_mismatch(gpu):
+    with pytest.raises(DimensionMismatch):
+        gsp.spmv(sp.identity(4, format="csr"), np.ones(5))
+
+
+@pytest.mark.parametrize("cfg,edge", [(1, 16), (2, 8), (3, 10), (4, 8)])
+def test_bsr_spmv_matches_scipy(gpu, cfg, edge):
+    s = synth.make_config(cfg, edge)
+    a = synth.to_scalar_csr(s, "cell", drop_zeros=False)
+    d = gsp.DeviceMatrix.from_bsr(s.rowptr, s.col, s.vals)
+    x = np.random.default_rng(cfg).standard_normal(s.n)
+    assert relerr(gsp.spmv(d, x), a @ x) <= 1e-14
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_spgemm_bitwise_scipy(gpu, seed):
+    """csr_matmat order, separate mul/add, exact zeros dropped."""
+    rng = np.random.default_rng(100 + seed)
+    shapes = [(40, 30, 50, 0.2), (400, 300, 500, 0.02), (300, 300, 300, 0.3), (50, 2000, 50, 0.2)]
+    for n, k, m, dens in shapes:
+        a = rand_csr(rng, n, k, dens)
+        b = rand_csr(rng, k, m, dens)
+        got = gsp.matmul(a, b).to_scipy()
+        assert_bitwise(got, (a @ b).tocsr())
+
+
+def test_spgemm_drops_cancellation_zeros(gpu):
+    # the behaviour scipy actually has (reference test_sparse.py:111-116 asserts the opposite)
+    a = sp.csr_matrix(np.array([[1.0, 1.0], [1.0, -1.0]]))
+    b = sp.csr_matrix(np.array([[1.0, 1.0], [1.0, 1.0]]))
+    got = gsp.matmul(a, b).to_scipy()
+    assert got.nnz == 2
+    assert_bitwise(got, (a @ b).tocsr())
+
+
+def test_triple_product_and_transpose(gpu):
+    a = poisson2d(12)
+    rng = np.random.default_rng(5)
+    p = rand_csr(rng, a.shape[0], 40, 0.05)
+    got = gsp.triple_product(p.T.tocsr(), a, p).to_scipy()
+    assert_bitwise(got, (p.T.tocsr() @ (a @ p)).tocsr())
+    t = gsp.as_device(p).transpose().to_scipy()
+    assert_bitwise(t, p.T.tocsr())
+
+
+def test_extract_keeps_stored_zeros(gpu):
+    a = sp.csr_matrix((np.array([1.0, 0.0, 2.0, 3.0]), np.array([0, 1, 1, 2]), np.array([0, 2, 3, 4])),
+                      shape=(3, 3))
+    got = gsp.extract(a, [0, 2], [1, 2]).to_scipy()
+    want = a[[0, 2]][:, [1, 2]].tocsr()
+    assert_bitwise(got, want)
+    assert got.nnz == 2
+
+
+@pytest.mark.parametrize("cfg,edge", [(1, 32), (2, 10), (3, 12), (4, 8)])
+def test_block_scale_bitwise_oracle(gpu, cfg, edge):
+    s = synth.make_config(cfg, edge)
+    d = gsp.DeviceMatrix.from_bsr(s.rowptr, s.col, s.vals)
+    dinv_g, ahat_g = gsp.block_scale(d)
+    dinv_o, ahat_o = obs.block_scale(s)
+    _, _, dv = dinv_g.download()
+    np.testing.assert_array_equal(dv.reshape(dinv_o.shape).view(np.int64), dinv_o.view(np.int64))
+    assert_bitwise(ahat_g.to_scipy(), ahat_o)
+    v = np.random.default_rng(1).standard_normal(s.n)
+    np.testing.assert_array_equal(gsp.block_apply(dinv_g, v), obs.prescale(dinv_o, v))
+
+
+@pytest.mark.parametrize("kind", ["injective", "noninjective", "injection"])
+def test_build_rp_bitwise_oracle(gpu, kind):
+    rng = np.random.default_rng(0)
+    n = 40
+    a = rng.standard_normal((n, n)) * 0.3 * (rng.random((n, n)) < 0.3) + np.diag(rng.uniform(2, 4, n))
+    A = sp.csr_matrix(a)
+    f = np.sort(rng.choice(n, 15, replace=False))
+    c = np.setdiff1d(np.arange(n), f)
+    r_o, p_o = omgr.build_rp(A, f, c, omgr.RpKind(kind))
+    part = type("Part", (), {"f_points": f, "c_points": c})
+    r_g, p_g = gmgr.build_rp(A, part, gmgr.RpKind(kind))
+    assert_bitwise(r_g.to_scipy(), r_o)
+    assert_bitwise(p_g.to_scipy(), p_o)
+
+
+def test_build_rp_ideal_close(gpu):
+    rng = np.random.default_rng(1)
+    n = 30
+    a = rng.standard_normal((n, n)) * 0.3 + np.diag(rng.uniform(2, 4, n)) * 5
+    A = sp.csr_matrix(a)
+    f = np.arange(0, n, 3)
+    c = np.setdiff1d(np.arange(n), f)
+    r_o, p_o = omgr.build_rp(A, f, c, omgr.RpKind.IDEAL)
+    part = type("Part", (), {"f_points": f, "c_points": c})
+    r_g, p_g = gmgr.build_rp(A, part, gmgr.RpKind.IDEAL)
+    assert np.max(np.abs(r_g.to_dense() - r_o.toarray())) < 1e-13
+    assert np.max(np.abs(p_g.to_dense() - p_o.toarray())) < 1e-13
+
+
+def test_build_rp_zero_f_diagonal_raises(gpu):
+    a = np.eye(4)
+    a[1, 1] = 0.0
+    a[1, 2] = 1.0
+    a[2, 1] = 1.0
+    part = type("Part", (), {"f_points": np.array([0, 1]), "c_points": np.array([2, 3])})
+    with pytest.raises(ZeroFDiagonal) as ei:
+        gmgr.build_rp(sp.csr_matrix(a), part, gmgr.RpKind.INJECTIVE)
+    assert ei.value.row == 1

@@ -1,0 +1,176 @@
+"""GPU parity: MGR setup/apply, GMRES, and the end-to-end synthetic solve.
+
+Mirrors tests/test_mgr.py (:101-170, 190-250) and tests/test_krylov.py of the
+reference with the oracle as the checker.  End-to-end bar (BASELINE.json):
+GMRES iterations within +-1 and solution within 1e-8 relative at rtol 1e-10.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from helpers import assert_bitwise, relerr
+from oracle import amg as oamg
+from oracle import blockscale as obs
+from oracle import krylov as okr
+from oracle import mgr as omgr
+from oracle import pipeline as opipe
+from paper_1801_08464_b200 import amg as gamg
+from paper_1801_08464_b200 import krylov as gkr
+from paper_1801_08464_b200 import mgr as gmgr
+from paper_1801_08464_b200 import pipeline as gpipe
+from paper_1801_08464_b200 import sparse as gsp
+from paper_1801_08464_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def random_system(rng, n):
+    a = rng.standard_normal((n, n)) * 0.3
+    a += np.diag(rng.uniform(2.0, 4.0, n)) * np.sqrt(n)
+    return a
+
+
+def spec_pair(kind, frelax, **fr):
+    return (omgr.MgrLevelSpec((), omgr.RpKind(kind), omgr.FRelax(frelax, **fr)),
+            gmgr.MgrLevelSpec((), gmgr.RpKind(kind), gmgr.FRelax(frelax, **fr)))
+
+
+@pytest.mark.parametrize("kind", ["injective", "noninjective", "injection"])
+@pytest.mark.parametrize("post", [False, True])
+def test_mgr_apply_exact_coarse(gpu, kind, post):
+    rng = np.random.default_rng(4)
+    n = 60
+    A = sp.csr_matrix(random_system(rng, n))
+    f = np.sort(rng.choice(n, 24, replace=False))
+    so, sg = spec_pair(kind, "jacobi", sweeps=2)
+    ho = omgr.setup_from_matrix(A, [(f, so)], coarse="exact", post_smoothing=post)
+    hg = gmgr.setup_from_matrix(A, [(f, sg)], coarse="exact", post_smoothing=post)
+    assert hg.level_dims() == ho.level_dims()
+    r = rng.standard_normal(n)
+    assert relerr(gmgr.mgr_apply(hg, r), omgr.mgr_apply(ho, r)) <= 1e-12
+    assert_bitwise(hg.coarse_operator().to_scipy(), ho.levels[-1].coarse_a)
+
+
+def test_ideal_exact_one_iteration(gpu):
+    rng = np.random.default_rng(2)
+    for _ in range(5):
+        n = int(rng.integers(8, 100))
+        A = sp.csr_matrix(random_system(rng, n))
+        nf = int(rng.integers(1, n))
+        f = np.sort(rng.choice(n, nf, replace=False))
+        spec = gmgr.MgrLevelSpec((), gmgr.RpKind.IDEAL, gmgr.FRelax("exact"))
+        h = gmgr.setup_from_matrix(A, [(f, spec)], coarse="exact")
+        b = rng.standard_normal(n)
+        res = gkr.gmres(A, h, b, gkr.GmresOptions(rel_tol=1e-10, max_iter=10, restart=10))
+        assert res.converged and res.iterations == 1
+
+
+def test_mgr_zero_and_linearity(gpu):
+    rng = np.random.default_rng(3)
+    n = 30
+    A = sp.csr_matrix(random_system(rng, n))
+    spec = gmgr.MgrLevelSpec((), gmgr.RpKind.NONINJECTIVE, gmgr.FRelax("jacobi", sweeps=2))
+    h = gmgr.setup_from_matrix(A, [(np.arange(10), spec)], coarse="exact")
+    np.testing.assert_array_equal(gmgr.mgr_apply(h, np.zeros(n)), np.zeros(n))
+    r1, r2 = rng.standard_normal(n), rng.standard_normal(n)
+    lhs = gmgr.mgr_apply(h, r1 + r2)
+    rhs = gmgr.mgr_apply(h, r1) + gmgr.mgr_apply(h, r2)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * max(np.max(np.abs(rhs)), 1.0)
+
+
+def test_empty_levels_skipped(gpu):
+    rng = np.random.default_rng(9)
+    n = 20
+    A = sp.csr_matrix(random_system(rng, n))
+    _, sg = spec_pair("injective", "jacobi")
+    h = gmgr.setup_from_matrix(A, [(np.array([], dtype=int), sg), (np.arange(n), sg), (np.arange(5), sg)],
+                               coarse="exact")
+    assert h.level_dims() == [20, 15]
+
+
+@pytest.mark.parametrize("cfg,edge", [(1, 24), (2, 10), (3, 10), (4, 6)])
+def test_synthetic_hierarchy_bitwise(gpu, cfg, edge):
+    """MGR level operators, R/P and both AMG hierarchies equal the oracle bit for bit."""
+    s = synth.make_config(cfg, edge)
+    _, ahat_o = obs.block_scale(s)
+    opts_kw = dict(gpipe.DEFAULT_AMG)
+    plan_o = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
+    ho = omgr.setup_from_matrix(ahat_o, plan_o, oamg.AmgOptions(**opts_kw))
+    d = gsp.DeviceMatrix.from_bsr(s.rowptr, s.col, s.vals)
+    _, ahat_g = gsp.block_scale(d)
+    hg = gmgr.setup_from_matrix(ahat_g, gpipe.default_plan(s.b, s.n_cells), gamg.AmgOptions(**opts_kw))
+    assert hg.level_dims() == ho.level_dims()
+    for k, lvl in enumerate(ho.levels):
+        assert_bitwise(hg.level_matrix(k, "r").to_scipy(), lvl.r)
+        assert_bitwise(hg.level_matrix(k, "p").to_scipy(), lvl.p)
+        assert_bitwise(hg.level_matrix(k, "coarse_a").to_scipy(), lvl.coarse_a)
+        fo = lvl.f_solver.hier
+        fg = hg.amg(k)
+        assert fg.level_sizes() == fo.level_sizes()
+        for q in range(len(fo.levels)):
+            assert_bitwise(fg.levels[q].a.to_scipy(), fo.levels[q].a.m)
+    co, cg = ho.coarse_amg, hg.amg(-1)
+    assert cg.level_sizes() == co.level_sizes()
+    for q in range(len(co.levels) - 1):
+        np.testing.assert_array_equal(cg.levels[q].splitting, co.levels[q].splitting)
+        assert_bitwise(cg.levels[q].p.to_scipy(), co.levels[q].p.m)
+    r = np.random.default_rng(0).standard_normal(s.n)
+    assert relerr(gmgr.mgr_apply(hg, r), omgr.mgr_apply(ho, r)) <= 1e-12
+
+
+def test_gmres_unpreconditioned_matches_oracle(gpu):
+    rng = np.random.default_rng(11)
+    n = 200
+    A = sp.csr_matrix(random_system(rng, n) / np.sqrt(n))
+    b = rng.standard_normal(n)
+    for opts in (dict(rel_tol=1e-10, restart=30, max_iter=400), dict(rel_tol=1e-10, restart=5, max_iter=40),
+                 dict(rel_tol=1e-8, restart=30, max_iter=400, reorthogonalize=False)):
+        ro = okr.gmres(lambda v: A @ v, None, b, okr.GmresOptions(**opts))
+        rg = gkr.gmres(A, None, b, gkr.GmresOptions(**opts))
+        assert abs(rg.iterations - ro.iterations) <= 1
+        assert rg.converged == ro.converged
+        assert relerr(rg.x, ro.x) <= 1e-8
+
+
+def test_gmres_zero_rhs_and_true_residual(gpu):
+    A = sp.identity(10, format="csr") * 2.0
+    r = gkr.gmres(A, None, np.zeros(10), gkr.GmresOptions())
+    assert r.iterations == 0 and r.converged
+    rng = np.random.default_rng(1)
+    M = sp.csr_matrix(random_system(rng, 40))
+    b = rng.standard_normal(40)
+    res = gkr.gmres(M, None, b, gkr.GmresOptions(rel_tol=1e-9))
+    assert res.converged
+    assert np.linalg.norm(b - M @ res.x) <= 1e-9 * np.linalg.norm(b) * (1 + 1e-6)
+
+
+def test_gmres_backward_error_acceptance(gpu):
+    rng = np.random.default_rng(2)
+    n = 60
+    A = sp.csr_matrix(random_system(rng, n))
+    b = rng.standard_normal(n)
+    a_norm = float(np.max(np.abs(A).sum(axis=1)))
+    ro = okr.gmres(lambda v: A @ v, None, b, okr.GmresOptions(rel_tol=1e-6, check_every=2), a_norm=a_norm)
+    rg = gkr.gmres(A, None, b, gkr.GmresOptions(rel_tol=1e-6, check_every=2), a_norm=a_norm)
+    assert abs(rg.iterations - ro.iterations) <= 1 and rg.converged
+
+
+def test_gmres_rejects_callables(gpu):
+    with pytest.raises(TypeError):
+        gkr.gmres(lambda v: v, None, np.ones(3))
+
+
+@pytest.mark.parametrize("cfg,edge", [(1, 32), (2, 10), (3, 10), (4, 6)])
+def test_end_to_end_parity(gpu, cfg, edge):
+    """Iterations within +-1, solution within 1e-8 at rtol 1e-10 (north-star bar)."""
+    s = synth.make_config(cfg, edge)
+    opts = oamg.AmgOptions(**gpipe.DEFAULT_AMG)
+    plan_o = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
+    ro, _, _ = opipe.solve_synthetic(s, rel_tol=1e-10, plan=plan_o, amg_opts=opts)
+    solver = gpipe.SyntheticSolver(rel_tol=1e-10)
+    rg, st = solver.solve_system(s)
+    assert ro.converged and rg.converged
+    assert abs(rg.iterations - ro.iterations) <= 1, (rg.iterations, ro.iterations)
+    assert relerr(rg.x, ro.x) <= 1e-8
+    a = synth.to_scalar_csr(s, "cell", drop_zeros=False)
+    assert np.linalg.norm(s.rhs - a @ rg.x) <= 1e-10 * np.linalg.norm(s.rhs) * (1 + 1e-6)
