@@ -1,0 +1,369 @@
+"""Benchmark: solved DOFs/s of MGR-GMRES (fp64, rtol 1e-8) on BASELINE config 3.
+
+One step = one linear system solved end to end on the device: per-cell block
+scaling, MGR + AMG setup, GMRES(30) to rtol 1e-8 (SURVEY.md §8(d) metric:
+n / (t_setup + t_solve)).  ``value`` is measured with the matrix and rhs
+already resident in HBM; ``e2e`` repeats the step through the public API
+with host buffers (pinned host -> device upload of A and b, device -> host
+read of x inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--edge 128]
+    python bench.py --impl reference ...   # CPU oracle port on the host cores
+
+Multi-GPU: replicas only (the solve does not shard); each
+rank solves its own system, time = max over ranks, scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "solved DOFs/s (MGR-GMRES fp64, rtol 1e-8)"
+UNIT = "DOF/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=3)
+    p.add_argument("--edge", type=int, default=None)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-edge", type=int, default=32)
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 7:
+                continue
+            for k, nm in enumerate(names):
+                if r[3 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(edge, config, seconds=10.0):
+    """Oracle port (numpy/scipy + C restatement) on one host core, bounded sample."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import pipeline as opipe
+    from oracle import amg as oamg, mgr as omgr
+    from paper_1801_08464_b200 import pipeline as gpipe, synth
+    s = synth.make_config(config, edge)
+    plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
+    opts = oamg.AmgOptions(**gpipe.DEFAULT_AMG)
+    t0 = time.perf_counter()
+    dofs, its, runs = 0, [], 0
+    while True:
+        res, _, tm = opipe.solve_synthetic(s, rel_tol=1e-8, plan=plan, amg_opts=opts)
+        dofs += s.n
+        its.append(res.iterations)
+        runs += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    return {"value": dofs / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"config-{config} generator at {edge}^3 ({s.n} DOFs), {runs} solve(s) in {el:.1f}s, "
+                      f"{its[-1]} GMRES its, oracle (numpy/scipy + C restatement)"}
+
+
+def reference_arm(args, ws, rank):
+    """--impl reference: the CPU oracle port with all host cores (process replicas)."""
+    cfg_edge = args.cpu_edge
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    ncpu = os.cpu_count() or 1
+    from paper_1801_08464_b200 import synth
+    n = synth.make_config(args.config, cfg_edge).n
+    ctxmp = mp.get_context("fork")
+    with ctxmp.Pool(ncpu) as pool:
+        for _ in range(args.warmup if args.warmup < 1 else 1):
+            pool.map(_ref_one, [(args.config, cfg_edge)] * ncpu)
+        t0 = time.perf_counter()
+        its = []
+        for _ in range(args.steps):
+            its += pool.map(_ref_one, [(args.config, cfg_edge)] * ncpu)
+        el = time.perf_counter() - t0
+    value = n * ncpu * args.steps / el
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"config-{args.config} generator, bounded sample {cfg_edge}^3 per process",
+                       "parallelism": f"{ncpu} independent CPU processes"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": ncpu, "kind": "port",
+                             "sample": f"{ncpu} concurrent solves of the config-{args.config} generator at "
+                                       f"{cfg_edge}^3 per step, GMRES its {min(its)}-{max(its)}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _ref_one(a):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    cfg, edge = a
+    from oracle import pipeline as opipe
+    from oracle import amg as oamg, mgr as omgr
+    from paper_1801_08464_b200 import pipeline as gpipe, synth
+    s = synth.make_config(cfg, edge)
+    plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
+    res, _, _ = opipe.solve_synthetic(s, rel_tol=1e-8, plan=plan, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG))
+    return res.iterations
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        dist = tdist
+    if args.impl == "reference":
+        reference_arm(args, ws, rank)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    from paper_1801_08464_b200 import _lib, synth
+    from paper_1801_08464_b200.pipeline import SyntheticSolver
+    from paper_1801_08464_b200.sparse import DeviceMatrix
+
+    ctx = _lib.ctx(local)
+    edge = args.edge
+    sysm = synth.make_config(args.config, edge, seed=rank)
+    n = sysm.n
+    solver = SyntheticSolver(rel_tol=1e-8, restart=30, max_iter=400, ctx=ctx)
+    a = solver.upload(sysm)
+    # rhs resident in HBM
+    b_dev = _lib.P()
+    x_dev = _lib.P()
+    ctx.call("mg_dev_alloc", 8 * n, _lib.ctypes.byref(b_dev))
+    ctx.call("mg_dev_alloc", 8 * n, _lib.ctypes.byref(x_dev))
+    rhs = np.ascontiguousarray(sysm.rhs)
+    ctx.call("mg_memcpy_h2d", b_dev, _lib.ptr(rhs), 8 * n)
+    gopts = solver.gopts.to_c()
+    res = _lib.GmresRes()
+
+    def device_step():
+        solver.setup()
+        ctx.call("mg_gmres_dev", a.h, solver.hier.h, b_dev, x_dev, _lib.ctypes.byref(gopts), -1.0,
+                 _lib.ctypes.byref(res))
+
+    def barrier():
+        ctx.sync()
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        device_step()
+    barrier()
+    # ---- timed region (device-resident inputs) --------------------------------------
+    import torch  # CUDA events on the library's stream via the runtime API
+    clk = ClockSampler(local)
+    clk.start()
+    launches0 = ctx.launches
+    its = []
+    conv = True
+    setup_ms, solve_ms = [], []
+    ev = _Events(ctx)
+    ev.record_start()
+    for _ in range(args.steps):
+        device_step()
+        t = ctx.timing()
+        setup_ms.append(t.setup_ms)
+        solve_ms.append(t.solve_ms)
+        its.append(res.iterations)
+        conv &= bool(res.converged)
+    ev.record_stop()
+    barrier()
+    total_ms = ev.elapsed_ms()
+    clocks = clk.stop()
+    launches = ctx.launches - launches0
+    if dist:
+        tt = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    value = n * ws / (ms_step / 1e3)
+
+    # ---- per-kernel rooflines: one extra profiled step ------------------------------
+    ctx.set_profiling(True)
+    device_step()
+    t = ctx.timing()
+    ctx.set_profiling(False)
+    hbm, peak_kind = peaks()
+    spmv_gbs = t.spmv_bytes * t.spmv_calls / (t.spmv_ms * 1e-3) / 1e9 if t.spmv_ms else None
+    vc_gbs = t.vcycle_bytes * t.vcycle_calls / (t.vcycle_ms * 1e-3) / 1e9 if t.vcycle_ms else None
+    roofline = {"bound": "hbm", "kernel": "coarse-grid AMG V(2,2) cycle (L1-Jacobi CSR sweeps, R/P SpMV, "
+                                          "dense coarsest) on the MGR Schur operator",
+                "achieved": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": (vc_gbs / hbm) if vc_gbs else None,
+                "traffic": None, "peak_kind": peak_kind,
+                "bytes_per_launch": t.vcycle_bytes, "avg_launch_ms": t.vcycle_ms / max(t.vcycle_calls, 1)}
+    spmv_roof = {"bound": "hbm", "kernel": "BCSR b=2 SpMV (GMRES operator)", "achieved": spmv_gbs, "peak": hbm,
+                 "unit": "GB/s", "frac": (spmv_gbs / hbm) if spmv_gbs else None,
+                 "bytes_per_launch": t.spmv_bytes, "avg_launch_ms": t.spmv_ms / max(t.spmv_calls, 1)}
+
+    # ---- e2e through the public API with host buffers --------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(ctx, sysm, args, dist, barrier, local, ws)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_edge, args.config)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE config generator)",
+                "config": {"workload": f"BASELINE config {args.config}: {sysm.nx}x{sysm.ny}x{sysm.nz} b={sysm.b}, "
+                                       f"{n} DOFs, GMRES(30)+MGR rtol 1e-8",
+                           "dofs": n, "nnzb": sysm.nnzb, "l2": "inputs larger than L2 (BCSR A ~600 MB at 128^3)",
+                           "parallelism": f"replicas x{ws}"},
+                "iterations": its[-1], "converged": conv, "setup_ms": statistics.median(setup_ms),
+                "solve_ms": statistics.median(solve_ms),
+                "roofline": roofline, "roofline_spmv": spmv_roof,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+class _Events:
+    """CUDA events recorded on the library context's stream (mg_timer_start / stop)."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.ms = None
+
+    def record_start(self):
+        self.ctx.sync()
+        self.ctx.call("mg_timer_start")
+
+    def record_stop(self):
+        import ctypes
+        v = ctypes.c_double()
+        self.ctx.call("mg_timer_stop", ctypes.byref(v))
+        self.ms = v.value
+
+    def elapsed_ms(self):
+        return self.ms
+
+
+def _e2e(ctx, sysm, args, dist, barrier, local, ws):
+    from paper_1801_08464_b200 import _lib
+    from paper_1801_08464_b200.pipeline import SyntheticSolver
+    import torch
+    # pinned host copies of the step's inputs
+    rp = torch.from_numpy(np.ascontiguousarray(sysm.rowptr)).pin_memory().numpy()
+    ci = torch.from_numpy(np.ascontiguousarray(sysm.col)).pin_memory().numpy()
+    vals = torch.from_numpy(np.ascontiguousarray(sysm.vals)).pin_memory().numpy()
+    rhs = torch.from_numpy(np.ascontiguousarray(sysm.rhs)).pin_memory().numpy()
+    xh = torch.empty(sysm.n, dtype=torch.float64).pin_memory().numpy()
+    solver = SyntheticSolver(rel_tol=1e-8, restart=30, max_iter=400, ctx=ctx)
+    gopts = solver.gopts.to_c()
+    res = _lib.GmresRes()
+    from paper_1801_08464_b200.sparse import DeviceMatrix
+
+    def step():
+        a = DeviceMatrix.from_bsr(rp, ci, vals, ctx=ctx)
+        solver.a = a
+        solver.setup(a, sysm.b, sysm.n_cells)
+        ctx.call("mg_gmres", a.h, solver.hier.h, _lib.ptr(rhs), _lib.ptr(xh), _lib.ctypes.byref(gopts), -1.0,
+                 _lib.ctypes.byref(res))
+        a.free()
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    barrier()
+    el = (time.perf_counter() - t0) * 1e3
+    if dist:
+        tt = torch.tensor([el], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    ms = el / args.steps
+    h2d = rp.nbytes + ci.nbytes + vals.nbytes + rhs.nbytes
+    return {"value": sysm.n * ws / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(xh.nbytes)}
+
+
+if __name__ == "__main__":
+    main()

@@ -79,13 +79,16 @@ int mg_extract(mg_ctx *ctx, const mg_mat *a, const int64_t *rows, int nr, const 
                int nc, mg_mat **out);
 
 /* ---- per-cell block scaling (cf. mgr.py:212-242) ------- */
-/* from a BSR A: Dinv (per-cell inverse of the diagonal blocks, kept inside the
- * returned scaled matrix handle) and Ahat = D^-1 A as scalar CSR in cell-major
- * unknown order, diagonal blocks exactly I, zero entries of scaled
- * off-diagonal blocks dropped. Returns the first singular cell via
+/* from a BSR A: the per-cell prescale blocks G_i = Lambda_i D_i^-1 (D_i the
+ * diagonal block; Lambda the equilibration lambda_r = |D_i[0][r]| or the
+ * column max when zero; Lambda = I when equilibrate == 0) as a block-diagonal
+ * BSR, and Ahat = G A as scalar CSR in cell-major unknown order with
+ * diagonal blocks exactly diag(Lambda_i) and zero entries of the scaled
+ * off-diagonal blocks dropped.  Returns the first singular cell via
  * mg_last_error_row on MG_ERR_SINGULAR. */
-int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, mg_mat **dinv_out, mg_mat **ahat_out);
-/* z = Dinv v (per-cell b x b matvec) */
+int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, int equilibrate, mg_mat **dinv_out,
+                   mg_mat **ahat_out);
+/* z = G v (per-cell b x b matvec) */
 int mg_block_apply(mg_ctx *ctx, const mg_mat *dinv, const double *v, double *z);
 
 /* ---- MGR build_rp (mgr.py:117-156) ------------------------------------------ */
@@ -190,6 +193,9 @@ typedef struct {
   double spmv_bytes;     /* algorithmic bytes of one BCSR SpMV */
 } mg_timing;
 int mg_get_timing(mg_ctx *ctx, mg_timing *t);
+/* CUDA-event timer on the context stream (bench timed regions) */
+int mg_timer_start(mg_ctx *ctx);
+int mg_timer_stop(mg_ctx *ctx, double *ms);
 int mg_set_profiling(mg_ctx *ctx, int on);
 
 #ifdef __cplusplus

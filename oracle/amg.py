@@ -56,6 +56,7 @@ class AmgOptions:
     smoother: str = "l1_jacobi"
     max_elmts: int = 4
     seed: int = 0
+    restriction: str = "galerkin"
 
     def __post_init__(self):
         if not (0.0 < self.strength_theta < 1.0):
@@ -72,6 +73,8 @@ class AmgOptions:
             raise ValueError(f"unknown smoother {self.smoother!r}")
         if self.max_elmts < 0:
             raise ValueError("max_elmts must be >= 0")
+        if self.restriction not in ("galerkin", "transpose_interp"):
+            raise ValueError(f"unknown restriction {self.restriction!r}")
 
 
 @dataclass
@@ -213,7 +216,13 @@ def amg_setup(a, opts=None) -> AmgHierarchy:
         if nc == cur.n:
             break
         p = extended_interpolation(cur.a, strong, state, opts.max_elmts)
-        pt = p.m.T.tocsr()
+        if opts.restriction == "galerkin":
+            pt = p.m.T.tocsr()
+        else:
+            # R = (extended+i interpolation of A^T on the same C/F split)^T
+            at = CsrMatrix(cur.a.m.T.tocsr())
+            pt = extended_interpolation(at, strength_graph(at, opts.strength_theta), state,
+                                        opts.max_elmts).m.T.tocsr()
         coarse = CsrMatrix((pt @ (cur.a.m @ p.m)).tocsr())
         cur.p = p
         cur.splitting = state

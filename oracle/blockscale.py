@@ -14,6 +14,9 @@ np.linalg.inv — tests compare against that at <= 1e-12):
   diagonal 1.0 entries and drops off-diagonal-block entries equal to 0.0.
 * prescale z_i = Dinv_i v_i (k ascending) — the first stage of
   M^-1 v = MGR_Ahat(D^-1 v).
+* equilibration (default on): every "Dinv" above is G_i = Lambda_i D_i^-1,
+  g[r][k] = lambda_r * dinv[r][k] with lambda_r = |A_ii[0][r]| (else the
+  column max |A_ii[k][r]|); the pinned diagonal blocks become diag(lambda_i).
 """
 from __future__ import annotations
 
@@ -85,14 +88,40 @@ def _bmul(dl, a):
     return out
 
 
-def block_scale(sysm):
-    """(Dinv [N,b,b], Ahat scalar CSR cell-major) per the pinned rules."""
+def row_scale(db):
+    """Equilibration lambda_{i,r}: |A_ii[0][r]| (the pressure row's coefficient of
+    variable r) when nonzero, else max_k |A_ii[k][r]|."""
+    cm = np.abs(db).max(axis=1)
+    pr = np.abs(db[:, 0, :])
+    return np.where(pr != 0.0, pr, cm)
+
+
+def prescale_blocks(sysm, equilibrate=True):
+    """G_i = Lambda_i D_i^-1 (g[r][k] = lambda_r * dinv[r][k]); plain D^-1 without equilibration."""
+    db = diag_blocks(sysm)
+    dinv = block_inverse(db)
+    if not equilibrate:
+        return dinv, np.ones(db.shape[:2])
+    lam = row_scale(db)
+    return lam[:, :, None] * dinv, lam
+
+
+def block_scale(sysm, equilibrate=True):
+    """(G [N,b,b], Ahat scalar CSR cell-major) per the pinned rules.
+
+    Ahat = G A with G = Lambda D^-1: off-diagonal blocks G_i A_ij (k ascending,
+    separate multiply/add), diagonal blocks exactly diag(lambda_i) (D3).  The
+    equilibration Lambda undoes the row normalisation of D^-1 so each row keeps
+    its physical scale; without it the row-normalised Laplacian blocks make
+    Galerkin R = P^T AMG diverge on config 3.
+    """
     N, b = sysm.n_cells, sysm.b
-    dinv = block_inverse(diag_blocks(sysm))
+    g, lam = prescale_blocks(sysm, equilibrate)
+    dinv = g
     brow = np.repeat(np.arange(N), np.diff(sysm.rowptr))
     scaled = _bmul(dinv[brow], sysm.vals)
     is_d = sysm.col == brow
-    scaled[is_d] = np.eye(b)
+    scaled[is_d] = lam[:, :, None] * np.eye(b)[None]
     rr = np.arange(b)
     rows = (brow[:, None, None] * b + rr[None, :, None]) + 0 * rr[None, None, :]
     cols = (sysm.col.astype(np.int64)[:, None, None] * b + rr[None, None, :]) + 0 * rr[None, :, None]

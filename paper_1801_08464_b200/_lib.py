@@ -63,7 +63,7 @@ _SIGS = {
     "mg_triple_product": [P, P, P, P, ctypes.POINTER(P)],
     "mg_transpose": [P, P, ctypes.POINTER(P)],
     "mg_extract": [P, P, P, c_int, P, c_int, ctypes.POINTER(P)],
-    "mg_block_scale": [P, P, ctypes.POINTER(P), ctypes.POINTER(P)],
+    "mg_block_scale": [P, P, c_int, ctypes.POINTER(P), ctypes.POINTER(P)],
     "mg_block_apply": [P, P, P, P],
     "mg_build_rp": [P, P, P, c_int, ctypes.POINTER(P), ctypes.POINTER(P)],
     "mg_amg_setup": [P, P, ctypes.POINTER(AmgOpts), ctypes.POINTER(P)],
@@ -91,6 +91,8 @@ _SIGS = {
     "mg_memcpy_d2h": [P, P, P, c_int64],
     "mg_get_timing": [P, ctypes.POINTER(Timing)],
     "mg_set_profiling": [P, c_int],
+    "mg_timer_start": [P],
+    "mg_timer_stop": [P, ctypes.POINTER(c_double)],
 }
 
 EXPORTED = sorted(list(_SIGS) + ["mg_last_error", "mg_last_error_row", "mg_ctx_launches",

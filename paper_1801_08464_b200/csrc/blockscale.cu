@@ -44,22 +44,38 @@ __device__ __forceinline__ bool invert_block(const double *a, double *inv) {
   }
 }
 
+// equilibration lambda_r = |a[0][r]| if nonzero else max_k |a[k][r]| (oracle row_scale)
+template <int B>
+__device__ __forceinline__ double lambda_of(const double *a, int r) {
+  double p = fabs(a[r]);
+  if (p != 0.0) return p;
+  double m = 0.0;
+#pragma unroll
+  for (int k = 0; k < B; ++k) m = fmax(m, fabs(a[k * B + r]));
+  return m;
+}
+
+// G_i = Lambda_i D_i^-1 (or D_i^-1 when !equil), one thread per cell
 template <int B>
 __global__ void k_block_inv(int N, const int *rp, const int *ci, const double *v, double *dinv,
-                            int *diag_pos, int *bad) {
+                            int *bad, int equil) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   int dp = -1;
   for (int q = rp[i]; q < rp[i + 1]; ++q)
     if (ci[q] == i) { dp = q; break; }
-  diag_pos[i] = dp;
   double a[B * B], inv[B * B];
   if (dp < 0) { atomicMin(bad, i); return; }
 #pragma unroll
   for (int t = 0; t < B * B; ++t) a[t] = v[(int64_t)dp * B * B + t];
   if (!invert_block<B>(a, inv)) { atomicMin(bad, i); return; }
 #pragma unroll
-  for (int t = 0; t < B * B; ++t) dinv[(int64_t)i * B * B + t] = inv[t];
+  for (int r = 0; r < B; ++r) {
+    double lam = equil ? lambda_of<B>(a, r) : 1.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      dinv[(int64_t)i * B * B + r * B + k] = equil ? __dmul_rn(lam, inv[r * B + k]) : inv[r * B + k];
+  }
 }
 
 // scaled entry (r, c) of block q in block row i: sum_k Dinv_i[r][k] * A_q[k][c]
@@ -74,7 +90,7 @@ __device__ __forceinline__ double scaled(const double *d, const double *a, int r
 // one thread per scalar row (cell i, var r): mode 0 count, mode 1 fill
 template <int B>
 __global__ void k_scale_rows(int N, const int *rp, const int *ci, const double *v, const double *dinv,
-                             int mode, int *cnt, const int *orp, int *oci, double *ov) {
+                             int mode, int *cnt, const int *orp, int *oci, double *ov, int equil) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)N * B) return;
   int i = (int)(t / B), r = (int)(t % B);
@@ -86,7 +102,10 @@ __global__ void k_scale_rows(int N, const int *rp, const int *ci, const double *
   for (int q = rp[i]; q < rp[i + 1]; ++q) {
     int j = ci[q];
     if (j == i) {
-      if (mode) { oci[o + c0] = i * B + r; ov[o + c0] = 1.0; }
+      if (mode) {
+        oci[o + c0] = i * B + r;
+        ov[o + c0] = equil ? lambda_of<B>(v + (int64_t)q * B * B, r) : 1.0;
+      }
       ++c0;
       continue;
     }
@@ -128,21 +147,22 @@ __global__ void k_diag_pattern(int N, int *rp, int *ci) {
   if (i == N) rp[N] = N;
 }
 
-void block_scale(const Csr &a, Csr &dinv, Csr &ahat) {
+void block_scale(const Csr &a, Csr &dinv, Csr &ahat, bool equil) {
   const int B = a.b;
   if (B != 2 && B != 3) throw MgError(MG_ERR_UNSUPPORTED, "block_scale: b must be 2 or 3");
   if (a.nr != a.nc) throw MgError(MG_ERR_DIM_MISMATCH, "block_scale: square block matrix required");
   int N = a.nr;
+  int eq = equil ? 1 : 0;
   dinv.alloc(N, N, N, B);
   k_diag_pattern<<<grid_for((int64_t)N + 1, 256), 256, 0, stream()>>>(N, dinv.rp.p, dinv.ci.p);
   check_launch("diag_pattern");
-  DBuf<int> dpos(N), bad(1);
+  DBuf<int> bad(1);
   int big = 0x7fffffff;
   h2d(bad.p, &big, sizeof(int));
   if (B == 2)
-    k_block_inv<2><<<grid_for(N, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, dpos.p, bad.p);
+    k_block_inv<2><<<grid_for(N, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, bad.p, eq);
   else
-    k_block_inv<3><<<grid_for(N, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, dpos.p, bad.p);
+    k_block_inv<3><<<grid_for(N, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, bad.p, eq);
   check_launch("block_inv");
   int hb = 0;
   d2h(&hb, bad.p, sizeof(int));
@@ -152,19 +172,18 @@ void block_scale(const Csr &a, Csr &dinv, Csr &ahat) {
   ahat.nr = ahat.nc = (int)n;
   ahat.b = 1;
   ahat.rp.alloc((size_t)n + 1);
-  if (B == 2)
-    k_scale_rows<2><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 0, cnt.p, nullptr, nullptr, nullptr);
-  else
-    k_scale_rows<3><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 0, cnt.p, nullptr, nullptr, nullptr);
-  check_launch("scale_count");
+  auto launch = [&](int mode, int *c, const int *orp, int *oci, double *ov) {
+    if (B == 2)
+      k_scale_rows<2><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, mode, c, orp, oci, ov, eq);
+    else
+      k_scale_rows<3><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, mode, c, orp, oci, ov, eq);
+    check_launch("scale_rows");
+  };
+  launch(0, cnt.p, nullptr, nullptr, nullptr);
   ahat.nnz = exclusive_scan_i32_to_i32(cnt.p, ahat.rp.p, (int)n);
   ahat.ci.alloc((size_t)ahat.nnz);
   ahat.v.alloc((size_t)ahat.nnz);
-  if (B == 2)
-    k_scale_rows<2><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 1, nullptr, ahat.rp.p, ahat.ci.p, ahat.v.p);
-  else
-    k_scale_rows<3><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, 1, nullptr, ahat.rp.p, ahat.ci.p, ahat.v.p);
-  check_launch("scale_fill");
+  launch(1, nullptr, ahat.rp.p, ahat.ci.p, ahat.v.p);
 }
 
 void block_apply(const Csr &dinv, const double *x, double *z) {

@@ -3,6 +3,6 @@
 #include "common.cuh"
 namespace mg {
 // dinv: block-diagonal BSR (N blocks); ahat: scalar CSR cell-major
-void block_scale(const Csr &a, Csr &dinv, Csr &ahat);
+void block_scale(const Csr &a, Csr &dinv, Csr &ahat, bool equilibrate);
 void block_apply(const Csr &dinv, const double *x, double *z);
 }  // namespace mg

@@ -242,11 +242,11 @@ int mg_extract(mg_ctx *ctx, const mg_mat *a, const int64_t *rows, int nr, const 
   });
 }
 
-int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, mg_mat **dinv_out, mg_mat **ahat_out) {
+int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, int equilibrate, mg_mat **dinv_out, mg_mat **ahat_out) {
   return guard(ctx, [&] {
     auto d = std::make_unique<mg_mat>();
     auto ah = std::make_unique<mg_mat>();
-    block_scale(a_bsr->m, d->m, ah->m);
+    block_scale(a_bsr->m, d->m, ah->m, equilibrate != 0);
     *dinv_out = d.release();
     *ahat_out = ah.release();
   });
@@ -516,6 +516,27 @@ int mg_memcpy_h2d(mg_ctx *ctx, void *dst, const void *src, int64_t bytes) {
 }
 int mg_memcpy_d2h(mg_ctx *ctx, void *dst, const void *src, int64_t bytes) {
   return guard(ctx, [&] { d2h(dst, src, (size_t)bytes); });
+}
+
+int mg_timer_start(mg_ctx *ctx) {
+  return guard(ctx, [&] {
+    if (!ctx->c.ev0) {
+      MG_CUDA(cudaEventCreate(&ctx->c.ev0));
+      MG_CUDA(cudaEventCreate(&ctx->c.ev1));
+    }
+    MG_CUDA(cudaEventRecord(ctx->c.ev0, stream()));
+  });
+}
+
+int mg_timer_stop(mg_ctx *ctx, double *ms) {
+  return guard(ctx, [&] {
+    if (!ctx->c.ev0) throw MgError(MG_ERR_BAD_OPTION, "mg_timer_start was not called");
+    MG_CUDA(cudaEventRecord(ctx->c.ev1, stream()));
+    MG_CUDA(cudaEventSynchronize(ctx->c.ev1));
+    float f = 0.f;
+    MG_CUDA(cudaEventElapsedTime(&f, ctx->c.ev0, ctx->c.ev1));
+    *ms = f;
+  });
 }
 
 int mg_get_timing(mg_ctx *ctx, mg_timing *t) {

@@ -1,5 +1,8 @@
 // Context-level helpers: stream-ordered allocation, copies, CUB scans.
 #include "common.cuh"
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 namespace mg {
@@ -26,6 +29,22 @@ void dfree(void *p, size_t bytes) {
 }
 
 void sync() { MG_CUDA(cudaStreamSynchronize(g_ctx->stream)); }
+
+void trace(const char *what) {
+  static int on = -1;
+  static std::chrono::steady_clock::time_point last;
+  if (on < 0) {
+    const char *e = getenv("MG_TRACE");
+    on = e && *e && *e != '0';
+    last = std::chrono::steady_clock::now();
+  }
+  if (!on) return;
+  sync();
+  auto now = std::chrono::steady_clock::now();
+  double ms = std::chrono::duration<double, std::milli>(now - last).count();
+  fprintf(stderr, "[mg] %-40s %9.3f ms  (dev mem %.2f GiB)\n", what, ms, g_ctx->dev_bytes / 1073741824.0);
+  last = std::chrono::steady_clock::now();
+}
 
 void h2d(void *dst, const void *src, size_t bytes) {
   if (!bytes) return;

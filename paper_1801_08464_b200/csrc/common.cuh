@@ -44,8 +44,7 @@ struct Ctx {
   size_t hbuf_cap = 0;
   void *cub_tmp = nullptr;
   size_t cub_cap = 0;
-  int *dflag = nullptr;         // device int scratch (4 ints)
-  int *hflag = nullptr;         // pinned mirror
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // mg_timer_start / mg_timer_stop
 };
 
 inline cudaStream_t stream() { return g_ctx->stream; }
@@ -120,6 +119,9 @@ inline int grid_for(int64_t work, int block, int max_blocks = 0) {
   if (g > 2147483647LL) g = 2147483647LL;
   return (int)g;
 }
+
+// MG_TRACE=1: synchronise and print the wall time since the previous mark
+void trace(const char *what);
 
 // host <-> device helpers (synchronous on the ctx stream)
 void h2d(void *dst, const void *src, size_t bytes);

@@ -86,18 +86,25 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
   while (h->L.back().n > o.cutoff && (int)h->L.size() < o.max_levels) {
     int li = (int)h->L.size() - 1;
     AmgLevel &cur = h->L[li];
+    trace("amg level start");
     DBuf<int8_t> s;
     if (strength(cur.A, o.theta, s) == 0) break;  // no strong connection: no progress
+    trace("  strength");
     DBuf<int8_t> state;
     pmis(cur.A, s.p, o.seed, li, state);
+    trace("  pmis");
     DBuf<int> cmap;
     int nc = coarse_map(state.p, cur.n, cmap);
     if (nc == 0) throw MgError(MG_ERR_AMG_SETUP, "coarsening produced an empty C set");
     if (nc == cur.n) break;
     Csr p = ext_interp(cur.A, s.p, state.p, cmap.p, nc, o.max_elmts);
+    trace("  ext_interp");
     Csr r = transpose(p);
+    trace("  transpose");
     Csr ap = spgemm(cur.A, p);
+    trace("  A*P");
     Csr ac = spgemm(r, ap);
+    trace("  R*(AP)");
     cur.P = std::move(p);
     cur.R = std::move(r);
     cur.split = std::move(state);
@@ -339,6 +346,7 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "mgr_setup: scalar CSR required");
   if (a.nr != a.nc) throw MgError(MG_ERR_DIM_MISMATCH, "mgr_setup: square matrix required");
   if (coarse_kind != 0 && coarse_kind != 1) throw MgError(MG_ERR_BAD_OPTION, "unknown coarse solver");
+  trace("mgr: enter");
   auto h = std::make_unique<Mgr>();
   h->n0 = a.nr;
   h->post_smoothing = post_smoothing;
@@ -359,11 +367,17 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
     h2d(mask.p, sp.fmask.data(), n);
     DBuf<int> fmap, cmap;
     fc_split(mask.p, n, lv.flist, lv.clist, fmap, cmap, lv.nf, lv.nc);
+    trace("mgr: fc_split");
     build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
+    trace("mgr: build_rp");
     Csr ap = spgemm(cur, lv.P);
+    trace("mgr: A*P");
     Csr ac = spgemm(lv.R, ap);
+    trace("mgr: R*(AP)");
     lv.Aff = extract(cur, lv.flist.p, lv.nf, fmap.p, lv.nf);
+    trace("mgr: extract A_ff");
     fsolver_setup(lv.fs, lv.Aff, sp, ao);
+    trace("mgr: F-solver setup");
     if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
     std::vector<int64_t> nxt_cells;
     {
@@ -382,8 +396,10 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
     cur = std::move(ac);
     h->L.push_back(std::move(lv));
   }
+  trace("mgr: levels done");
   if (coarse_kind == 0) {
     h->camg = amg_setup(cur, ao);
+    trace("mgr: coarse AMG setup");
   } else {
     if (cur.nr > DENSE_LIMIT) throw MgError(MG_ERR_UNSUPPORTED, "coarse='exact' on the GPU is limited to n <= 8192");
     h->cn = cur.nr;

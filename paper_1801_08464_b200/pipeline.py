@@ -26,7 +26,7 @@ from .sparse import DeviceMatrix, block_scale
 
 # defaults used by bench.py, smoke() and the parity tests (oracle uses the same)
 DEFAULT_AMG = dict(strength_theta=0.25, pre_sweeps=2, post_sweeps=2, max_elmts=4)
-DEFAULT_FRELAX = dict(pre=2, post=2)
+DEFAULT_FRELAX = dict(pre=1, post=1)
 
 
 def default_amg_options(**kw) -> AmgOptions:

@@ -194,10 +194,12 @@ def extract(a, rows, cols) -> DeviceMatrix:
     return DeviceMatrix(d.ctx, h)
 
 
-def block_scale(a_bsr: DeviceMatrix):
-    """(Dinv, Ahat = D^-1 A) with exact identity diagonal blocks."""
+def block_scale(a_bsr: DeviceMatrix, equilibrate: bool = True):
+    """(G, Ahat = G A), G = Lambda D^-1 per cell, diagonal blocks exactly diag(Lambda)
+    (SURVEY.md §7 D2/D3 plus the row equilibration of DESIGN.md §4)."""
     d, ah = _lib.P(), _lib.P()
-    a_bsr.ctx.call("mg_block_scale", a_bsr.h, _lib.ctypes.byref(d), _lib.ctypes.byref(ah))
+    a_bsr.ctx.call("mg_block_scale", a_bsr.h, int(bool(equilibrate)), _lib.ctypes.byref(d),
+                   _lib.ctypes.byref(ah))
     return DeviceMatrix(a_bsr.ctx, d), DeviceMatrix(a_bsr.ctx, ah)
 
 
