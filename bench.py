@@ -47,13 +47,6 @@ def parse():
     return p.parse_args()
 
 
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -182,19 +175,12 @@ def _ref_one(a):
 
 def main():
     args = parse()
-    ws, rank, local = dist_env()
-    dist = None
-    if ws > 1:
-        import torch
-        import torch.distributed as tdist
-        torch.cuda.set_device(local)
-        tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
-        dist = tdist
+    from paper_1801_08464_b200.replicas import Replicas
+    rep = Replicas("nccl" if args.impl == "ours" else "gloo")
+    ws, rank, local = rep.world, rep.rank, rep.local
     if args.impl == "reference":
         reference_arm(args, ws, rank)
-        if dist:
-            dist.barrier()
-            dist.destroy_process_group()
+        rep.close()
         return
 
     from paper_1801_08464_b200 import _lib, synth
@@ -203,7 +189,7 @@ def main():
 
     ctx = _lib.ctx(local)
     edge = args.edge
-    sysm = synth.make_config(args.config, edge, seed=rank)
+    sysm = synth.make_config(args.config, edge, seed=rep.seed())
     n = sysm.n
     solver = SyntheticSolver(rel_tol=1e-8, restart=30, max_iter=400, ctx=ctx)
     a = solver.upload(sysm)
@@ -224,14 +210,12 @@ def main():
 
     def barrier():
         ctx.sync()
-        if dist:
-            dist.barrier()
+        rep.barrier()
 
     for _ in range(args.warmup):
         device_step()
     barrier()
     # ---- timed region (device-resident inputs) --------------------------------------
-    import torch  # CUDA events on the library's stream via the runtime API
     clk = ClockSampler(local)
     clk.start()
     launches0 = ctx.launches
@@ -252,10 +236,7 @@ def main():
     total_ms = ev.elapsed_ms()
     clocks = clk.stop()
     launches = ctx.launches - launches0
-    if dist:
-        tt = torch.tensor([total_ms], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
+    total_ms = rep.max(total_ms)
     ms_step = total_ms / args.steps
     value = n * ws / (ms_step / 1e3)
 
@@ -279,7 +260,7 @@ def main():
     # ---- e2e through the public API with host buffers --------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(ctx, sysm, args, dist, barrier, local, ws)
+        e2e = _e2e(ctx, sysm, args, rep, barrier)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -298,9 +279,7 @@ def main():
                 "roofline": roofline, "roofline_spmv": spmv_roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    rep.close()
 
 
 class _Events:
@@ -324,7 +303,7 @@ class _Events:
         return self.ms
 
 
-def _e2e(ctx, sysm, args, dist, barrier, local, ws):
+def _e2e(ctx, sysm, args, rep, barrier):
     from paper_1801_08464_b200 import _lib
     from paper_1801_08464_b200.pipeline import SyntheticSolver
     import torch
@@ -355,13 +334,10 @@ def _e2e(ctx, sysm, args, dist, barrier, local, ws):
         step()
     barrier()
     el = (time.perf_counter() - t0) * 1e3
-    if dist:
-        tt = torch.tensor([el], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        el = float(tt.item())
+    el = rep.max(el)
     ms = el / args.steps
     h2d = rp.nbytes + ci.nbytes + vals.nbytes + rhs.nbytes
-    return {"value": sysm.n * ws / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "h2d_bytes_per_step": int(h2d),
+    return {"value": sysm.n * rep.world / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(xh.nbytes)}
 
 
