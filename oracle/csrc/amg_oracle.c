@@ -110,6 +110,27 @@ int pmis(int n, const int *indptr, const int *indices, const int8_t *strong,
     return rounds;
 }
 
+/*
+ * Pinned summation order for the extended+i scalar sums: TREE(t_0..t_{m-1})
+ * = acc, acc = 0 then acc = acc + tree32(chunk) for each chunk of 32 terms
+ * (zero padded), tree32(w) = for off in 16,8,4,2,1: w[l] = w[l] + w[l+off]
+ * (l < off); return w[0].  This is the GPU's warp shuffle-down tree, so a
+ * warp can form these sums in parallel and still match bit for bit.
+ */
+static double tree32(const double *t, int n) {
+    double w[32];
+    for (int l = 0; l < 32; ++l) w[l] = l < n ? t[l] : 0.0;
+    for (int off = 16; off > 0; off >>= 1)
+        for (int l = 0; l < off; ++l) w[l] = w[l] + w[l + off];
+    return w[0];
+}
+
+static double tree_sum(const double *t, int m) {
+    double acc = 0.0;
+    for (int c = 0; c < m; c += 32) acc = acc + tree32(t + c, m - c < 32 ? m - c : 32);
+    return acc;
+}
+
 static double row_diag(const int *indptr, const int *indices, const double *data, int k) {
     double d = 0.0;
     for (int e = indptr[k]; e < indptr[k + 1]; ++e)
@@ -143,12 +164,14 @@ static int cmp_sel(const void *a, const void *b) {
  *   dt      = a_ii + sum_{weak n not in Chat_i} a_in
  *                  + sum_{k in F^s_i} (beta_k == 0 ? a_ik : (a_ik/beta_k)*abar_ki)
  *   w_ij    = -(a_ij + sum_k (a_ik/beta_k)*abar_kj) / dt   for j in Chat_i
- * Operation order: dt starts at a_ii, adds row-i lumps in column order, then
- * per strong-F k in row-i order either a_ik or f*abar_ki; num[j] starts at
- * 0, adds a_ij (if stored), then f*abar_kj per k in row-i order.
+ * Operation order: dt = a_ii + TREE(row-i lumps, row order), then per
+ * strong-F k in row-i order either + a_ik (beta_k == 0) or + f*abar_ki;
+ * beta_k = TREE(row k terms, row order); num[j] starts at 0, adds a_ij (if
+ * stored), then f*abar_kj per k in row-i order.  TREE is the warp tree sum
+ * defined at tree_sum() above.
  * Optional truncation to max_elmts largest |w| (ties: smaller column), kept
- * weights scaled by (sum all w)/(sum kept w) (both summed in column order)
- * when the kept sum is nonzero.
+ * weights scaled by TREE(all w)/TREE(kept w) (column order) when the kept
+ * sum is nonzero.
  * mode 0: count (cnt[i] = row length), mode 1: fill rows at p_indptr.
  * Columns are written as FINE indices (the caller maps to coarse ids).
  * Returns -1 on success, else the row with a zero interpolation pivot.
@@ -164,6 +187,8 @@ static int ext_interp_impl(int n, const int *indptr, const int *indices, const d
     int *chat = (int *)malloc(sizeof(int) * cap);
     double *num = (double *)malloc(sizeof(double) * cap);
     wsel_t *sel = (wsel_t *)malloc(sizeof(wsel_t) * cap);
+    int tcap = 64;
+    double *terms = (double *)malloc(sizeof(double) * tcap);
     int bad = -1;
     for (int i = 0; i < n && bad < 0; ++i) {
         if (state[i] == CPOINT) {
@@ -193,32 +218,52 @@ static int ext_interp_impl(int n, const int *indptr, const int *indices, const d
         if (mode == 0) { cnt[i] = outlen; continue; }
         qsort(chat, (size_t)m, sizeof(int), cmp_int);
         for (int q = 0; q < m; ++q) { pos[chat[q]] = q; num[q] = 0.0; }
-        double dt = row_diag(indptr, indices, data, i);
+        /* scratch for TREE sums (row lengths and m) */
+        int need = m;
+        for (int e = indptr[i]; e < indptr[i + 1]; ++e) {
+            int k = indices[e];
+            int len = indptr[k + 1] - indptr[k];
+            if (len > need) need = len;
+        }
+        if (indptr[i + 1] - indptr[i] > need) need = indptr[i + 1] - indptr[i];
+        if (need > tcap) { tcap = need; terms = (double *)realloc(terms, sizeof(double) * tcap); }
+        /* direct numerators */
         for (int e = indptr[i]; e < indptr[i + 1]; ++e) {
             int j = indices[e];
-            if (j == i) continue;
-            if (mark[j] == i) num[pos[j]] = num[pos[j]] + data[e];
-            else if (strong[e] && state[j] == FPOINT) continue;
-            else dt = dt + data[e];
+            if (j != i && mark[j] == i) num[pos[j]] = num[pos[j]] + data[e];
         }
+        /* dt = a_ii + TREE(weak lumps in row order) */
+        int nt = 0;
+        for (int e = indptr[i]; e < indptr[i + 1]; ++e) {
+            int j = indices[e];
+            double t = 0.0;
+            if (j != i && mark[j] != i && !(strong[e] && state[j] == FPOINT)) t = data[e];
+            terms[nt++] = t;
+        }
+        double dt = row_diag(indptr, indices, data, i) + tree_sum(terms, nt);
         for (int e = indptr[i]; e < indptr[i + 1]; ++e) {
             int k = indices[e];
             if (k == i || !strong[e] || state[k] != FPOINT) continue;
             double akk = row_diag(indptr, indices, data, k);
-            double beta = 0.0;
+            /* beta = TREE over row k of abar_kl, l in Chat u {i} */
+            nt = 0;
+            int at_i = -1;
             for (int e2 = indptr[k]; e2 < indptr[k + 1]; ++e2) {
                 int l = indices[e2];
-                if (l == k || !opposite(data[e2], akk)) continue;
-                if (l == i || mark[l] == i) beta = beta + data[e2];
+                double t = 0.0;
+                if (l != k && opposite(data[e2], akk) && (l == i || mark[l] == i)) t = data[e2];
+                if (l != k && l == i && opposite(data[e2], akk)) at_i = e2;
+                terms[nt++] = t;
             }
+            double beta = tree_sum(terms, nt);
             if (beta == 0.0) { dt = dt + data[e]; continue; }
             double f = data[e] / beta;
             for (int e2 = indptr[k]; e2 < indptr[k + 1]; ++e2) {
                 int l = indices[e2];
                 if (l == k || !opposite(data[e2], akk)) continue;
                 if (mark[l] == i) num[pos[l]] = num[pos[l]] + f * data[e2];
-                else if (l == i) dt = dt + f * data[e2];
             }
+            if (at_i >= 0) dt = dt + f * data[at_i];
         }
         if (dt == 0.0) { bad = i; break; }
         for (int q = 0; q < m; ++q) num[q] = -num[q] / dt;
@@ -226,16 +271,16 @@ static int ext_interp_impl(int n, const int *indptr, const int *indices, const d
         if (outlen == m) {
             for (int q = 0; q < m; ++q) { p_col[o + q] = chat[q]; p_val[o + q] = num[q]; }
         } else {
-            double s_all = 0.0;
-            for (int q = 0; q < m; ++q) s_all = s_all + num[q];
+            double s_all = tree_sum(num, m);
             for (int q = 0; q < m; ++q) { sel[q].absw = fabs(num[q]); sel[q].col = q; }
             qsort(sel, (size_t)m, sizeof(wsel_t), cmp_sel);
             /* kept positions, back in column order */
             int *keep = (int *)malloc(sizeof(int) * (size_t)outlen);
             for (int q = 0; q < outlen; ++q) keep[q] = sel[q].col;
             qsort(keep, (size_t)outlen, sizeof(int), cmp_int);
-            double s_kept = 0.0;
-            for (int q = 0; q < outlen; ++q) s_kept = s_kept + num[keep[q]];
+            for (int q = 0; q < m; ++q) terms[q] = 0.0;
+            for (int q = 0; q < outlen; ++q) terms[keep[q]] = num[keep[q]];
+            double s_kept = tree_sum(terms, m);
             double scale = s_kept != 0.0 ? s_all / s_kept : 1.0;
             for (int q = 0; q < outlen; ++q) {
                 p_col[o + q] = chat[keep[q]];
@@ -244,7 +289,7 @@ static int ext_interp_impl(int n, const int *indptr, const int *indices, const d
             free(keep);
         }
     }
-    free(mark); free(pos); free(chat); free(num); free(sel);
+    free(mark); free(pos); free(chat); free(num); free(sel); free(terms);
     return bad;
 }
 

@@ -261,6 +261,14 @@ int pmis(const Csr &a, const int8_t *s, uint64_t seed, int level, DBuf<int8_t> &
 }
 
 // ---- extended+i interpolation ----------------------------------------------------
+// Pinned warp tree sum (oracle tree32): w = v; for off in 16,8,4,2,1: w[l] += w[l+off];
+// result = w[0], broadcast to every lane.
+__device__ __forceinline__ double warp_tree(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+
 __device__ __forceinline__ bool opposite(double v, double dkk) {
   return (v < 0.0 && dkk > 0.0) || (v > 0.0 && dkk < 0.0);
 }
@@ -342,20 +350,26 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
     if (sl >= 0) { int p = t.pos[sl]; num[p] = __dadd_rn(num[p], v[q]); }
   }
   __syncwarp();
-  // dt: a_ii, then weak lumps in row order (sequential in lane 0)
-  double dt = 0.0;
-  if (lane == 0) {
-    for (int q = b; q < e; ++q)
-      if (ci[q] == i) dt = __dadd_rn(dt, v[q]);
-    for (int q = b; q < e; ++q) {
-      int j = ci[q];
-      if (j == i) continue;
-      if (hash_find_opt(t.keys, mask, j) >= 0) continue;
-      if (s[q] && state[j] == FPT) continue;
-      dt = __dadd_rn(dt, v[q]);
+  // dt = a_ii + TREE(weak lumps of row i): lanes classify, pinned warp tree
+  double dt;
+  {
+    int found = -1;
+    double lump = 0.0;
+    for (int q0 = b; q0 < e; q0 += 32) {
+      int q = q0 + lane;
+      double term = 0.0;
+      if (q < e) {
+        int j = ci[q];
+        if (j == i) found = q;
+        else if (hash_find_opt(t.keys, mask, j) < 0 && !(s[q] && state[j] == FPT)) term = v[q];
+      }
+      lump = __dadd_rn(lump, warp_tree(term));
     }
+    unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
+    double aii = bal ? __dadd_rn(0.0, v[__shfl_sync(0xffffffffu, found, __ffs(bal) - 1)]) : 0.0;
+    dt = __dadd_rn(aii, lump);
   }
-  // distribution through strong F neighbours k, in row order
+  // distribution through strong F neighbours k, in row-i order
   for (int q = b; q < e; ++q) {
     int k = ci[q];
     if (k == i || !s[q] || state[k] != FPT) continue;
@@ -366,21 +380,25 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
     for (int q2 = kb + lane; q2 < ke; q2 += 32)
       if (ci[q2] == k) found = q2;
     unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
-    double akk = 0.0;
-    if (bal) akk = __dadd_rn(0.0, v[__shfl_sync(0xffffffffu, found, __ffs(bal) - 1)]);
+    double akk = bal ? __dadd_rn(0.0, v[__shfl_sync(0xffffffffu, found, __ffs(bal) - 1)]) : 0.0;
+    // beta = TREE over row k of abar_kl for l in Chat u {i}
     double beta = 0.0;
-    if (lane == 0) {
-      for (int q2 = kb; q2 < ke; ++q2) {
+    int at_i = -1;
+    for (int q0 = kb; q0 < ke; q0 += 32) {
+      int q2 = q0 + lane;
+      double term = 0.0;
+      if (q2 < ke) {
         int l = ci[q2];
-        if (l == k) continue;
         double val = v[q2];
-        if (!opposite(val, akk)) continue;
-        if (l == i || hash_find_opt(t.keys, mask, l) >= 0) beta = __dadd_rn(beta, val);
+        if (l != k && opposite(val, akk)) {
+          if (l == i) { term = val; at_i = q2; }
+          else if (hash_find_opt(t.keys, mask, l) >= 0) term = val;
+        }
       }
+      beta = __dadd_rn(beta, warp_tree(term));
     }
-    beta = __shfl_sync(0xffffffffu, beta, 0);
     if (beta == 0.0) {
-      if (lane == 0) dt = __dadd_rn(dt, aik);
+      dt = __dadd_rn(dt, aik);
       continue;
     }
     double f = __ddiv_rn(aik, beta);
@@ -392,13 +410,10 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
       int sl = hash_find_opt(t.keys, mask, l);
       if (sl >= 0) { int p = t.pos[sl]; num[p] = __dadd_rn(num[p], __dmul_rn(f, val)); }
     }
-    if (lane == 0) {
-      for (int q2 = kb; q2 < ke; ++q2)
-        if (ci[q2] == i && opposite(v[q2], akk)) dt = __dadd_rn(dt, __dmul_rn(f, v[q2]));
-    }
+    unsigned bi = __ballot_sync(0xffffffffu, at_i >= 0);
+    if (bi) dt = __dadd_rn(dt, __dmul_rn(f, v[__shfl_sync(0xffffffffu, at_i, __ffs(bi) - 1)]));
     __syncwarp();
   }
-  dt = __shfl_sync(0xffffffffu, dt, 0);
   if (dt == 0.0) {
     if (lane == 0) atomicMin(A.bad, i);
     return;
@@ -433,11 +448,14 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
     if (lane == 0 && bq < u) flag[bq] = 1;
     __syncwarp();
   }
+  double s_all = 0.0, s_kept = 0.0;
+  for (int q0 = 0; q0 < u; q0 += 32) {
+    int q = q0 + lane;
+    double w_q = q < u ? num[q] : 0.0;
+    s_all = __dadd_rn(s_all, warp_tree(w_q));
+    s_kept = __dadd_rn(s_kept, warp_tree(q < u && flag[q] ? w_q : 0.0));
+  }
   if (lane == 0) {
-    double s_all = 0.0, s_kept = 0.0;
-    for (int q = 0; q < u; ++q) s_all = __dadd_rn(s_all, num[q]);
-    for (int q = 0; q < u; ++q)
-      if (flag[q]) s_kept = __dadd_rn(s_kept, num[q]);
     double scale = s_kept != 0.0 ? __ddiv_rn(s_all, s_kept) : 1.0;
     int w = 0;
     for (int q = 0; q < u; ++q)
@@ -453,7 +471,7 @@ template <int T, int WPB>
 __global__ void __launch_bounds__(WPB * 32) k_ext_smem(int nrows, const int *rows, ExtArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpTables t = carve(smem + table_bytes(T) * wid, T);
+  WarpTables t = carve(smem + table_bytes(T, false) * wid, T, false);
   for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB) ext_row(rows[r], T, t, lane, A);
 }
 __global__ void k_ext_gmem(int nrows, const int *rows, const int64_t *goff, const int *gsize,
@@ -461,13 +479,13 @@ __global__ void k_ext_gmem(int nrows, const int *rows, const int64_t *goff, cons
   int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= nrows) return;
   int T = gsize[wid];
-  ext_row(rows[wid], T, carve(pool + goff[wid], T), lane, A);
+  ext_row(rows[wid], T, carve(pool + goff[wid], T, false), lane, A);
 }
 
 template <int T, int WPB>
 static void launch_ext(int nrows, const int *rows, const ExtArgs &A) {
   if (!nrows) return;
-  size_t sm = table_bytes(T) * WPB;
+  size_t sm = table_bytes(T, false) * WPB;
   MG_CUDA(cudaFuncSetAttribute(k_ext_smem<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int grid = (nrows + WPB - 1) / WPB;
   int cap = g_ctx->num_sms * 16;
@@ -518,12 +536,16 @@ Csr ext_interp(const Csr &a, const int8_t *s, const int8_t *state, const int *cm
   bins.build(ub.p, n);
   ExtArgs A{a.rp.p, a.ci.p, a.v.p, s, state, cmap, max_elmts, 0, cnt.p, nullptr, nullptr, nullptr, bad.p};
   auto run = [&]() {
-    launch_ext<256, 8>(bins.cnt[0], bins.rows.p + bins.off[0], A);
-    launch_ext<1024, 4>(bins.cnt[1], bins.rows.p + bins.off[1], A);
-    launch_ext<4096, 2>(bins.cnt[2], bins.rows.p + bins.off[2], A);
-    int n3 = bins.cnt[3];
-    if (n3) {
-      k_ext_gmem<<<grid_for((int64_t)n3 * 32, 128), 128, 0, stream()>>>(n3, bins.rows.p + bins.off[3],
+    launch_ext<64, 8>(bins.cnt[0], bins.rows.p + bins.off[0], A);
+    launch_ext<128, 8>(bins.cnt[1], bins.rows.p + bins.off[1], A);
+    launch_ext<256, 8>(bins.cnt[2], bins.rows.p + bins.off[2], A);
+    launch_ext<512, 8>(bins.cnt[3], bins.rows.p + bins.off[3], A);
+    launch_ext<1024, 8>(bins.cnt[4], bins.rows.p + bins.off[4], A);
+    launch_ext<2048, 4>(bins.cnt[5], bins.rows.p + bins.off[5], A);
+    launch_ext<4096, 2>(bins.cnt[6], bins.rows.p + bins.off[6], A);
+    int ng = bins.cnt[NBIN];
+    if (ng) {
+      k_ext_gmem<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(ng, bins.rows.p + bins.off[NBIN],
                                                                          bins.goff.p, bins.gsize.p,
                                                                          bins.pool.p, A);
       check_launch("ext_gmem");

@@ -58,22 +58,53 @@ __device__ __forceinline__ void warp_bitonic(int *L, int P, int lane) {
 }
 
 struct WarpTables {
-  int *keys;    // T
-  int *pos;     // T
-  int *list;    // T/2
-  double *acc;  // T/2
+  int *keys;     // T
+  int *pos;      // T
+  int *list;     // T/2
+  double *acc;   // T/2
+  int *pcol;     // T/2  staged products / terms (column)
+  double *pval;  // T/2  staged products / terms (value)
 };
 
-// per-warp table bytes for T slots: acc (T/2 f64) | keys (T) | pos (T) | list (T/2)
-__host__ __device__ inline size_t table_bytes(int T) { return (size_t)T * 14; }
+// per-warp table bytes for T slots:
+// acc (T/2 f64) | [pval (T/2 f64)] | keys (T) | pos (T) | list (T/2) | [pcol (T/2)]
+// the bracketed staging arrays exist only when `staged` (small / medium rows)
+__host__ __device__ inline size_t table_bytes(int T, bool staged = true) {
+  return (size_t)T * (staged ? 20 : 14);
+}
 
-__device__ __forceinline__ WarpTables carve(unsigned char *w, int T) {
+__device__ __forceinline__ WarpTables carve(unsigned char *w, int T, bool staged = true) {
   WarpTables t;
   t.acc = (double *)w;
-  t.keys = (int *)(w + (size_t)T / 2 * 8);
+  t.pval = staged ? t.acc + T / 2 : nullptr;
+  t.keys = (int *)(t.acc + (staged ? T : T / 2));
   t.pos = t.keys + T;
   t.list = t.pos + T;
+  t.pcol = staged ? t.list + T / 2 : nullptr;
   return t;
+}
+
+// acc[pos(col[p])] += val[p] for p in [0, np) in index order (bit-exact sequential
+// order per accumulator): 32 staged products per step, lanes that hit the same
+// accumulator are serialised in lane order by their group leader.
+__device__ __forceinline__ void ordered_accumulate(WarpTables t, unsigned mask, int np, int lane) {
+  for (int c = 0; c < np; c += 32) {
+    int p = c + lane;
+    bool valid = p < np;
+    int pos = valid ? t.pos[hash_find(t.keys, mask, t.pcol[p])] : -1 - lane;
+    unsigned grp = __match_any_sync(0xffffffffu, pos);
+    if (valid && lane == __ffs(grp) - 1) {
+      double s = t.acc[pos];
+      unsigned m = grp;
+      while (m) {
+        int l = __ffs(m) - 1;
+        s = __dadd_rn(s, t.pval[c + l]);
+        m &= m - 1;
+      }
+      t.acc[pos] = s;
+    }
+    __syncwarp();
+  }
 }
 
 __device__ __forceinline__ void table_clear(WarpTables t, int T, int lane) {
@@ -100,17 +131,18 @@ __device__ __forceinline__ void table_sort(WarpTables t, int T, int u, int lane)
   __syncwarp();
 }
 
-// Row lists binned by an upper bound on the row's distinct keys:
-// bin 0: ub <= 128 (T=256), 1: <= 512 (T=1024), 2: <= 2048 (T=4096),
-// 3: global-memory tables with T = pow2 >= 2 ub.
+// Row lists binned by an upper bound ub on the row's staged entries / keys:
+// bin b < NBIN holds rows with ub <= 32 << b and uses T = 64 << b table slots;
+// bin NBIN (the last) uses global-memory tables with T = pow2 >= 2 ub.
+static const int NBIN = 7;   // smem bins up to ub <= 2048 (T = 4096)
 struct RowBins {
-  int cnt[4] = {0, 0, 0, 0};
-  int off[4] = {0, 0, 0, 0};
+  int cnt[NBIN + 1] = {};
+  int off[NBIN + 1] = {};
   DBuf<int> rows;          // all rows grouped by bin
-  DBuf<int> gsize;         // bin 3: table slots per row
-  DBuf<int64_t> goff;      // bin 3: byte offsets into pool
+  DBuf<int> gsize;         // global bin: table slots per row
+  DBuf<int64_t> goff;      // global bin: byte offsets into pool
   DBuf<unsigned char> pool;
-  void build(const int *ub_dev, int m);
+  void build(const int *ub_dev, int m, bool staged_global = false);
 };
 
 }  // namespace mg

@@ -29,30 +29,84 @@ static __device__ void spgemm_row(int row, int T, WarpTables t, int lane, const 
   table_clear(t, T, lane);
   int s = arp[row], e = arp[row + 1];
   int mine = 0;
-  for (int q = s + lane; q < e; q += 32) {
-    int j = aci[q];
-    for (int r = brp[j]; r < brp[j + 1]; ++r) mine += hash_insert(t.keys, mask, bci[r]);
+  if (mode == 0) {
+    for (int q = s + lane; q < e; q += 32) {
+      int j = aci[q];
+      for (int r = brp[j]; r < brp[j + 1]; ++r) mine += hash_insert(t.keys, mask, bci[r]);
+    }
+    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+    if (lane == 0) cnt[row] = mine;
+    return;
+  }
+  if (!t.pcol) {
+    // large rows: no staging buffer; j ascending, lanes over B_j
+    for (int q = s + lane; q < e; q += 32) {
+      int j = aci[q];
+      for (int r = brp[j]; r < brp[j + 1]; ++r) mine += hash_insert(t.keys, mask, bci[r]);
+    }
+    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+    int u = mine;
+    __syncwarp();
+    table_sort(t, T, u, lane);
+    for (int q = lane; q < u; q += 32) t.acc[q] = 0.0;
+    __syncwarp();
+    for (int q = s; q < e; ++q) {
+      int j = aci[q];
+      double a = av[q];
+      for (int r = brp[j] + lane; r < brp[j + 1]; r += 32) {
+        int p = t.pos[hash_find(t.keys, mask, bci[r])];
+        t.acc[p] = __dadd_rn(t.acc[p], __dmul_rn(a, bv[r]));
+      }
+      __syncwarp();
+    }
+    int64_t o = base[row];
+    int nzc = 0;
+    for (int q = lane; q < u; q += 32) {
+      oci[o + q] = t.list[q];
+      double val = t.acc[q];
+      ov[o + q] = val;
+      nzc += val != 0.0;
+    }
+    for (int off = 16; off > 0; off >>= 1) nzc += __shfl_xor_sync(0xffffffffu, nzc, off);
+    if (lane == 0) nz[row] = nzc;
+    return;
+  }
+  // stage every product a_ij*b_jk in (j, k) stored order: lanes own consecutive
+  // entries of A's row, a warp scan of |B_j| gives each lane its output offset
+  int np = 0;
+  for (int q0 = s; q0 < e; q0 += 32) {
+    int q = q0 + lane;
+    int j = 0, rb = 0, re = 0;
+    double a = 0.0;
+    if (q < e) {
+      j = aci[q];
+      a = av[q];
+      rb = brp[j];
+      re = brp[j + 1];
+    }
+    int len = re - rb, incl = len;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    int o = np + incl - len;
+    for (int r = rb; r < re; ++r, ++o) {
+      int k = bci[r];
+      t.pcol[o] = k;
+      t.pval[o] = __dmul_rn(a, bv[r]);
+      mine += hash_insert(t.keys, mask, k);
+    }
+    np += __shfl_sync(0xffffffffu, incl, 31);
   }
   for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
   int u = mine;
   __syncwarp();
-  if (mode == 0) {
-    if (lane == 0) cnt[row] = u;
-    return;
-  }
   table_sort(t, T, u, lane);
   for (int q = lane; q < u; q += 32) t.acc[q] = 0.0;
   __syncwarp();
-  // ordered accumulation: j ascending (left row order), lanes over B_j
-  for (int q = s; q < e; ++q) {
-    int j = aci[q];
-    double a = av[q];
-    for (int r = brp[j] + lane; r < brp[j + 1]; r += 32) {
-      int p = t.pos[hash_find(t.keys, mask, bci[r])];
-      t.acc[p] = __dadd_rn(t.acc[p], __dmul_rn(a, bv[r]));
-    }
-    __syncwarp();
-  }
+  // ordered accumulation: 0 + p_1 + p_2 + ... in staged (= scipy) order per column
+  ordered_accumulate(t, mask, np, lane);
   int64_t o = base[row];
   int nzc = 0;
   for (int q = lane; q < u; q += 32) {
@@ -65,7 +119,7 @@ static __device__ void spgemm_row(int row, int T, WarpTables t, int lane, const 
   if (lane == 0) nz[row] = nzc;
 }
 
-template <int T, int WPB>
+template <int T, int WPB, bool STAGED>
 __global__ void __launch_bounds__(WPB * 32) k_spgemm_smem(int nrows, const int *rows, const int *arp,
                                                           const int *aci, const double *av,
                                                           const int *brp, const int *bci,
@@ -74,7 +128,7 @@ __global__ void __launch_bounds__(WPB * 32) k_spgemm_smem(int nrows, const int *
                                                           int *nz) {
   extern __shared__ __align__(16) unsigned char smem[];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpTables t = carve(smem + table_bytes(T) * wid, T);
+  WarpTables t = carve(smem + table_bytes(T, STAGED) * wid, T, STAGED);
   for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB)
     spgemm_row(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, mode, cnt, base, oci, ov, nz);
 }
@@ -87,7 +141,7 @@ __global__ void k_spgemm_gmem(int nrows, const int *rows, const int64_t *tab_off
   int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= nrows) return;
   int T = tab_size[wid];
-  WarpTables t = carve(pool + tab_off[wid], T);
+  WarpTables t = carve(pool + tab_off[wid], T, false);
   spgemm_row(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, mode, cnt, base, oci, ov, nz);
 }
 
@@ -125,27 +179,46 @@ __global__ void k_row_ub(int m, const int *arp, const int *aci, const int *brp, 
   if (lane == 0) ub[wid] = s > 0x3fffffff ? 0x3fffffff : (int)s;
 }
 
-__device__ __forceinline__ int bin_of(int v) { return v <= 128 ? 0 : v <= 512 ? 1 : v <= 2048 ? 2 : 3; }
+__device__ __forceinline__ int bin_of(int v) {
+  int b = 0;
+  while (b < NBIN && v > (32 << b)) ++b;
+  return b;
+}
 
+// per-block bin histogram in shared memory, one global atomic per bin per block
 __global__ void k_bin_count(int m, const int *ub, int *bin_cnt) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) atomicAdd(&bin_cnt[bin_of(ub[i])], 1);
+  __shared__ int h[NBIN + 1];
+  if (threadIdx.x <= NBIN) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[bin_of(ub[i])], 1);
+  __syncthreads();
+  if (threadIdx.x <= NBIN && h[threadIdx.x]) atomicAdd(&bin_cnt[threadIdx.x], h[threadIdx.x]);
 }
+// stable within a block: block-local ranks, one global reservation per bin per block
 __global__ void k_bin_fill(int m, const int *ub, int *fillpos, int *rows) {
+  __shared__ int h[NBIN + 1], base[NBIN + 1];
+  if (threadIdx.x <= NBIN) h[threadIdx.x] = 0;
+  __syncthreads();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  int b = bin_of(ub[i]);
-  int p = atomicAdd(&fillpos[b], 1);
-  rows[p] = i;
+  int b = -1, r = 0;
+  if (i < m) {
+    b = bin_of(ub[i]);
+    r = atomicAdd(&h[b], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x <= NBIN && h[threadIdx.x]) base[threadIdx.x] = atomicAdd(&fillpos[threadIdx.x], h[threadIdx.x]);
+  __syncthreads();
+  if (b >= 0) rows[base[b] + r] = i;
 }
-__global__ void k_gmem_tabs(int nr, const int *rows, const int *ub, int *tsz, int *units) {
+__global__ void k_gmem_tabs(int nr, const int *rows, const int *ub, int *tsz, int *units, int staged) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nr) return;
   int u = ub[rows[i]];
   int T = 64;
   while (T < 2 * u) T <<= 1;
   tsz[i] = T;
-  units[i] = (int)(((int64_t)T * 14 + 15) / 16);  // 16-byte units
+  units[i] = (int)((table_bytes(T, staged != 0) + 15) / 16);  // 16-byte units
 }
 
 __global__ void k_scale_i64(int64_t *a, int64_t s, int n) {
@@ -157,46 +230,48 @@ void scale_i64(int64_t *a, int64_t s, int n) {
   check_launch("scale_i64");
 }
 
-void RowBins::build(const int *ub_dev, int m) {
-  DBuf<int> bc(4);
-  dzero(bc.p, sizeof(int) * 4);
+void RowBins::build(const int *ub_dev, int m, bool staged_global) {
+  DBuf<int> bc(NBIN + 1);
+  dzero(bc.p, sizeof(int) * (NBIN + 1));
   if (m) {
-    k_bin_count<<<grid_for(m, 256), 256, 0, stream()>>>(m, ub_dev, bc.p);
+    k_bin_count<<<grid_for(m, 256, g_ctx->num_sms * 4), 256, 0, stream()>>>(m, ub_dev, bc.p);
     check_launch("bin_count");
   }
-  d2h(cnt, bc.p, sizeof(int) * 4);
+  d2h(cnt, bc.p, sizeof(int) * (NBIN + 1));
   off[0] = 0;
-  for (int b = 1; b < 4; ++b) off[b] = off[b - 1] + cnt[b - 1];
-  h2d(bc.p, off, sizeof(int) * 4);
+  for (int b = 1; b <= NBIN; ++b) off[b] = off[b - 1] + cnt[b - 1];
+  h2d(bc.p, off, sizeof(int) * (NBIN + 1));
   rows.alloc((size_t)(m ? m : 1));
   if (m) {
     k_bin_fill<<<grid_for(m, 256), 256, 0, stream()>>>(m, ub_dev, bc.p, rows.p);
     check_launch("bin_fill");
   }
-  int n3 = cnt[3];
-  if (n3) {
-    gsize.alloc(n3);
-    DBuf<int> units(n3);
-    goff.alloc((size_t)n3 + 1);
-    k_gmem_tabs<<<grid_for(n3, 256), 256, 0, stream()>>>(n3, rows.p + off[3], ub_dev, gsize.p, units.p);
+  int ng = cnt[NBIN];
+  if (ng) {
+    gsize.alloc(ng);
+    DBuf<int> units(ng);
+    goff.alloc((size_t)ng + 1);
+    k_gmem_tabs<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, rows.p + off[NBIN], ub_dev, gsize.p, units.p,
+                                                          staged_global ? 1 : 0);
     check_launch("gmem_tabs");
-    int64_t tot = exclusive_scan_i32_to_i64(units.p, goff.p, n3);
+    int64_t tot = exclusive_scan_i32_to_i64(units.p, goff.p, ng);
     pool.alloc((size_t)tot * 16);
-    scale_i64(goff.p, 16, n3 + 1);
+    scale_i64(goff.p, 16, ng + 1);
   }
 }
 
-template <int T, int WPB>
+template <int T, int WPB, bool STAGED>
 static void launch_bin(int nrows, const int *rows, const Csr &a, const Csr &b, int mode, int *cnt,
                        const int64_t *base, int *oci, double *ov, int *nz) {
   if (!nrows) return;
-  size_t sm = table_bytes(T) * WPB;
-  MG_CUDA(cudaFuncSetAttribute(k_spgemm_smem<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  size_t sm = table_bytes(T, STAGED) * WPB;
+  MG_CUDA(cudaFuncSetAttribute(k_spgemm_smem<T, WPB, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm));
   int grid = (nrows + WPB - 1) / WPB;
   int cap = g_ctx->num_sms * 16;
   if (grid > cap) grid = cap;
-  k_spgemm_smem<T, WPB><<<grid, WPB * 32, sm, stream()>>>(nrows, rows, a.rp.p, a.ci.p, a.v.p, b.rp.p,
-                                                          b.ci.p, b.v.p, mode, cnt, base, oci, ov, nz);
+  k_spgemm_smem<T, WPB, STAGED><<<grid, WPB * 32, sm, stream()>>>(nrows, rows, a.rp.p, a.ci.p, a.v.p, b.rp.p,
+                                                                  b.ci.p, b.v.p, mode, cnt, base, oci, ov, nz);
   check_launch("spgemm_smem");
 }
 
@@ -216,13 +291,20 @@ Csr spgemm(const Csr &a, const Csr &b) {
   RowBins bins;
   bins.build(ub.p, m);
   auto run = [&](int mode, const int64_t *base, int *oci, double *ov) {
-    launch_bin<256, 8>(bins.cnt[0], bins.rows.p + bins.off[0], a, b, mode, cnt.p, base, oci, ov, nz.p);
-    launch_bin<1024, 4>(bins.cnt[1], bins.rows.p + bins.off[1], a, b, mode, cnt.p, base, oci, ov, nz.p);
-    launch_bin<4096, 2>(bins.cnt[2], bins.rows.p + bins.off[2], a, b, mode, cnt.p, base, oci, ov, nz.p);
-    int n3 = bins.cnt[3];
-    if (n3) {
-      k_spgemm_gmem<<<grid_for((int64_t)n3 * 32, 128), 128, 0, stream()>>>(
-          n3, bins.rows.p + bins.off[3], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, a.v.p,
+#define BIN(k, T, W, S) \
+    launch_bin<T, W, S>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, mode, cnt.p, base, oci, ov, nz.p)
+    BIN(0, 64, 8, true);
+    BIN(1, 128, 8, true);
+    BIN(2, 256, 8, true);
+    BIN(3, 512, 8, true);
+    BIN(4, 1024, 4, true);
+    BIN(5, 2048, 2, true);
+    BIN(6, 4096, 2, false);
+#undef BIN
+    int ng = bins.cnt[NBIN];
+    if (ng) {
+      k_spgemm_gmem<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
+          ng, bins.rows.p + bins.off[NBIN], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, a.v.p,
           b.rp.p, b.ci.p, b.v.p, mode, cnt.p, base, oci, ov, nz.p);
       check_launch("spgemm_gmem");
     }

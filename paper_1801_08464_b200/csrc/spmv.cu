@@ -29,75 +29,119 @@ struct EpiJacobi {
   __device__ void operator()(int i, double s) const { xo[i] = x[i] + dinv[i] * (b[i] - s); }
 };
 
-// VS lanes cooperate on one row; every lane runs the shuffle (no early exit).
-template <int VS, class Epi>
+// VS lanes cooperate on one row; each lane keeps U independent (value, column)
+// loads in flight before the dependent x gathers, so a warp has VS*U*12 B of
+// matrix traffic outstanding per round trip.  Groups stride over rows (grid
+// sized to the resident capacity); every lane runs the shuffle (uniform loop).
+template <int VS, int U, class Epi>
 __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ rp,
                                              const int *__restrict__ ci,
                                              const double *__restrict__ v,
                                              const double *__restrict__ x, Epi epi) {
-  int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int row = (int)(tid / VS);
-  int lane = (int)(tid % VS);
-  double sum = 0.0;
-  if (row < nr) {
-    int s = __ldg(rp + row), e = __ldg(rp + row + 1);
-#pragma unroll 4
-    for (int k = s + lane; k < e; k += VS) sum += __ldg(v + k) * __ldg(x + __ldg(ci + k));
-  }
+  const int lane = threadIdx.x % VS;
+  const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VS);
+  const int ng = (int)((int64_t)gridDim.x * blockDim.x / VS);
+  const int warp_first = (int)(((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / VS);
+  for (int row = g0, wf = warp_first; wf < nr; row += ng, wf += ng) {
+    double sum = 0.0;
+    if (row < nr) {
+      int s = __ldg(rp + row), e = __ldg(rp + row + 1);
+      for (int k0 = s; k0 < e; k0 += VS * U) {
+        double vv[U];
+        int cc[U];
 #pragma unroll
-  for (int off = VS / 2; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off, VS);
-  if (row < nr && lane == 0) epi(row, sum);
+        for (int u = 0; u < U; ++u) {
+          int k = k0 + lane + u * VS;
+          bool ok = k < e;
+          vv[u] = ok ? __ldcs(v + k) : 0.0;
+          cc[u] = ok ? __ldcs(ci + k) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (cc[u] >= 0) sum += vv[u] * __ldg(x + cc[u]);
+      }
+    }
+#pragma unroll
+    for (int off = VS / 2; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off, VS);
+    if (row < nr && lane == 0) epi(row, sum);
+  }
 }
 
-template <int B, int G>
+template <int B, int G, int U>
 __global__ void __launch_bounds__(256) k_bsr(int nbr, const int *__restrict__ rp,
                                              const int *__restrict__ ci,
                                              const double *__restrict__ v,
                                              const double *__restrict__ x,
                                              double *__restrict__ y) {
-  int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int row = (int)(tid / G);
-  int lane = (int)(tid % G);
-  double acc[B];
+  const int lane = threadIdx.x % G;
+  const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
+  const int ng = (int)((int64_t)gridDim.x * blockDim.x / G);
+  const int warp_first = (int)(((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / G);
+  for (int row = g0, wf = warp_first; wf < nbr; row += ng, wf += ng) {
+    double acc[B];
 #pragma unroll
-  for (int r = 0; r < B; ++r) acc[r] = 0.0;
-  if (row < nbr) {
-    int s = __ldg(rp + row), e = __ldg(rp + row + 1);
-    for (int k = s + lane; k < e; k += G) {
-      int c = __ldg(ci + k);
-      if (B == 2) {
-        const double2 *vb = reinterpret_cast<const double2 *>(v) + (int64_t)k * 2;
-        double2 r0 = __ldg(vb), r1 = __ldg(vb + 1);
-        double2 xc = __ldg(reinterpret_cast<const double2 *>(x) + c);
-        acc[0] += r0.x * xc.x + r0.y * xc.y;
-        acc[1] += r1.x * xc.x + r1.y * xc.y;
-      } else {
-        const double *vb = v + (int64_t)k * B * B;
-        double xc[B];
+    for (int r = 0; r < B; ++r) acc[r] = 0.0;
+    if (row < nbr) {
+      int s = __ldg(rp + row), e = __ldg(rp + row + 1);
+      for (int k0 = s; k0 < e; k0 += G * U) {
+        double a[U][B * B];
+        int cc[U];
 #pragma unroll
-        for (int q = 0; q < B; ++q) xc[q] = __ldg(x + (int64_t)c * B + q);
+        for (int u = 0; u < U; ++u) {
+          int k = k0 + lane + u * G;
+          cc[u] = k < e ? __ldcs(ci + k) : -1;
+          if (B == 2) {
+            const double2 *vb = reinterpret_cast<const double2 *>(v) + (int64_t)(k < e ? k : s) * 2;
+            double2 r0 = __ldcs(vb), r1 = __ldcs(vb + 1);
+            a[u][0] = r0.x; a[u][1] = r0.y; a[u][2] = r1.x; a[u][3] = r1.y;
+          } else {
+            const double *vb = v + (int64_t)(k < e ? k : s) * B * B;
 #pragma unroll
-        for (int r = 0; r < B; ++r) {
-          double t = 0.0;
+            for (int q = 0; q < B * B; ++q) a[u][q] = __ldcs(vb + q);
+          }
+        }
 #pragma unroll
-          for (int q = 0; q < B; ++q) t += __ldg(vb + r * B + q) * xc[q];
-          acc[r] += t;
+        for (int u = 0; u < U; ++u) {
+          if (cc[u] < 0) continue;
+          double xc[B];
+          if (B == 2) {
+            double2 t = __ldg(reinterpret_cast<const double2 *>(x) + cc[u]);
+            xc[0] = t.x; xc[1] = t.y;
+          } else {
+#pragma unroll
+            for (int q = 0; q < B; ++q) xc[q] = __ldg(x + (int64_t)cc[u] * B + q);
+          }
+#pragma unroll
+          for (int r = 0; r < B; ++r) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < B; ++q) t += a[u][r * B + q] * xc[q];
+            acc[r] += t;
+          }
         }
       }
     }
-  }
 #pragma unroll
-  for (int r = 0; r < B; ++r)
+    for (int r = 0; r < B; ++r)
 #pragma unroll
-    for (int off = G / 2; off > 0; off >>= 1) acc[r] += __shfl_down_sync(0xffffffffu, acc[r], off, G);
-  if (row < nbr && lane == 0) {
-    if (B == 2) {
-      reinterpret_cast<double2 *>(y)[row] = make_double2(acc[0], acc[1]);
-    } else {
+      for (int off = G / 2; off > 0; off >>= 1) acc[r] += __shfl_down_sync(0xffffffffu, acc[r], off, G);
+    if (row < nbr && lane == 0) {
+      if (B == 2) {
+        reinterpret_cast<double2 *>(y)[row] = make_double2(acc[0], acc[1]);
+      } else {
 #pragma unroll
-      for (int r = 0; r < B; ++r) y[(int64_t)row * B + r] = acc[r];
+        for (int r = 0; r < B; ++r) y[(int64_t)row * B + r] = acc[r];
+      }
     }
   }
+}
+
+// resident-capacity grid for the row-striding SpMV kernels
+static int spmv_grid(int64_t threads_needed) {
+  int64_t want = (threads_needed + 255) / 256;
+  int64_t cap = (int64_t)g_ctx->num_sms * 8;
+  if (want > cap) want = cap;
+  return (int)(want < 1 ? 1 : want);
 }
 
 template <class Epi>
@@ -106,14 +150,17 @@ static void launch_csr(const Csr &a, const double *x, Epi epi) {
   double avg = a.nr ? (double)a.nnz / a.nr : 0.0;
   const int T = 256;
   cudaStream_t s = stream();
-#define LAUNCH(VS)                                                                    \
-  k_csr<VS, Epi><<<grid_for((int64_t)a.nr * VS, T), T, 0, s>>>(a.nr, a.rp.p, a.ci.p, \
-                                                               a.v.p, x, epi)
-  if (avg <= 2.5) LAUNCH(2);
-  else if (avg <= 5) LAUNCH(4);
-  else if (avg <= 12) LAUNCH(8);
-  else if (avg <= 28) LAUNCH(16);
-  else LAUNCH(32);
+  (void)T;
+#define LAUNCH(VS, U)                                                               \
+  k_csr<VS, U, Epi><<<spmv_grid((int64_t)a.nr * VS), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, \
+                                                                  a.v.p, x, epi)
+  if (avg <= 2.5) LAUNCH(2, 2);
+  else if (avg <= 5) LAUNCH(4, 2);
+  else if (avg <= 9) LAUNCH(4, 3);
+  else if (avg <= 18) LAUNCH(8, 3);
+  else if (avg <= 36) LAUNCH(16, 3);
+  else if (avg <= 72) LAUNCH(16, 5);
+  else LAUNCH(32, 4);
 #undef LAUNCH
   check_launch("csr spmv");
 }
@@ -127,12 +174,13 @@ void spmv(const Csr &a, const double *x, double *y) {
   const int T = 256;
   double avg = (double)a.nnz / a.nr;
   cudaStream_t s = stream();
+  (void)T;
   if (a.b == 2) {
-    if (avg <= 4.5) k_bsr<2, 4><<<grid_for((int64_t)a.nr * 4, T), T, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
-    else k_bsr<2, 8><<<grid_for((int64_t)a.nr * 8, T), T, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    if (avg <= 4.5) k_bsr<2, 2, 3><<<spmv_grid((int64_t)a.nr * 2), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    else k_bsr<2, 4, 2><<<spmv_grid((int64_t)a.nr * 4), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
   } else if (a.b == 3) {
-    if (avg <= 4.5) k_bsr<3, 4><<<grid_for((int64_t)a.nr * 4, T), T, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
-    else k_bsr<3, 8><<<grid_for((int64_t)a.nr * 8, T), T, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    if (avg <= 4.5) k_bsr<3, 2, 3><<<spmv_grid((int64_t)a.nr * 2), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    else k_bsr<3, 4, 2><<<spmv_grid((int64_t)a.nr * 4), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
   } else {
     throw MgError(MG_ERR_UNSUPPORTED, "block size must be 1, 2 or 3");
   }
