@@ -120,10 +120,11 @@ int mg_ctx_destroy(mg_ctx *ctx) {
   {
     Enter e(ctx);
     cudaStreamSynchronize(ctx->c.stream);
-    if (ctx->c.red) cudaFreeAsync(ctx->c.red, ctx->c.stream);
-    if (ctx->c.cub_tmp) cudaFreeAsync(ctx->c.cub_tmp, ctx->c.stream);
     if (ctx->c.hbuf) cudaFreeHost(ctx->c.hbuf);
-    cudaStreamSynchronize(ctx->c.stream);
+    alloc_release_cache(&ctx->c);
+    for (auto &kv : ctx->c.block_size) cudaFree(kv.first);  // blocks still owned by live handles
+    ctx->c.block_size.clear();
+    if (ctx->c.ev0) { cudaEventDestroy(ctx->c.ev0); cudaEventDestroy(ctx->c.ev1); }
     cudaStreamDestroy(ctx->c.stream);
   }
   delete ctx;

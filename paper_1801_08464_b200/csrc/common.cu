@@ -9,23 +9,66 @@ namespace mg {
 
 thread_local Ctx *g_ctx = nullptr;
 
+// Caching allocator: best-fit free list of cudaMalloc blocks, never returned
+// to the driver until the context is destroyed (or an allocation fails).  All
+// work is ordered on the context's single stream, so a freed block can be
+// reused by the next allocation immediately.  This keeps setup / solve times
+// free of driver allocation stalls (the stream-ordered pool showed 2-3x
+// step-to-step variance from physical-memory remapping).
+static size_t round_size(size_t b) {
+  if (b <= ((size_t)1 << 20)) return (b + 511) & ~(size_t)511;
+  return (b + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
+}
+
+void alloc_release_cache(Ctx *c) {
+  cudaStreamSynchronize(c->stream);
+  for (auto &kv : c->free_blocks) cudaFree(kv.second);
+  c->cached_bytes = 0;
+  c->free_blocks.clear();
+}
+
 void *dmalloc(size_t bytes) {
   if (!bytes) return nullptr;
+  Ctx *c = g_ctx;
+  size_t rb = round_size(bytes);
+  auto it = c->free_blocks.lower_bound(rb);
+  if (it != c->free_blocks.end() && it->first <= rb * 2 + ((size_t)4 << 20)) {
+    void *p = it->second;
+    size_t sz = it->first;
+    c->free_blocks.erase(it);
+    c->cached_bytes -= sz;
+    c->block_size[p] = sz;
+    c->dev_bytes += (int64_t)sz;
+    return p;
+  }
   void *p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, bytes, g_ctx->stream);
+  cudaError_t e = cudaMalloc(&p, rb);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    alloc_release_cache(c);
+    e = cudaMalloc(&p, rb);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw MgError(MG_ERR_CUDA, std::string("device allocation of ") + std::to_string(bytes) +
                                    " bytes failed: " + cudaGetErrorString(e));
   }
-  g_ctx->dev_bytes += (int64_t)bytes;
+  c->block_size[p] = rb;
+  c->dev_bytes += (int64_t)rb;
   return p;
 }
 
 void dfree(void *p, size_t bytes) {
+  (void)bytes;
   if (!p) return;
-  cudaFreeAsync(p, g_ctx->stream);
-  g_ctx->dev_bytes -= (int64_t)bytes;
+  Ctx *c = g_ctx;
+  auto it = c->block_size.find(p);
+  if (it == c->block_size.end()) return;
+  size_t sz = it->second;
+  c->block_size.erase(it);
+  c->dev_bytes -= (int64_t)sz;
+  c->free_blocks.emplace(sz, p);
+  c->cached_bytes += sz;
 }
 
 void sync() { MG_CUDA(cudaStreamSynchronize(g_ctx->stream)); }

@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 #include <stdexcept>
 #include <cstring>
@@ -45,7 +47,13 @@ struct Ctx {
   void *cub_tmp = nullptr;
   size_t cub_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // mg_timer_start / mg_timer_stop
+  // caching allocator state (common.cu)
+  std::multimap<size_t, void *> free_blocks;
+  std::unordered_map<void *, size_t> block_size;
+  size_t cached_bytes = 0;
 };
+
+void alloc_release_cache(Ctx *c);
 
 inline cudaStream_t stream() { return g_ctx->stream; }
 inline void count_launch(int n = 1) { g_ctx->launches += n; }
