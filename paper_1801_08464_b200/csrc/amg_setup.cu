@@ -302,6 +302,32 @@ struct ExtArgs {
   int *bad;
 };
 
+// insert Chat_i = C^s_i u (C^s_k for strong-F k) into keys (initialised to -1);
+// returns |Chat_i| on every lane.  Lanes own consecutive entries of row i; for
+// strong-F k they walk row k (each lane its own k).
+__device__ __forceinline__ int ext_candidates(int i, int *keys, unsigned mask, int lane, const ExtArgs &A) {
+  const int *rp = A.rp, *ci = A.ci;
+  const int8_t *s = A.s, *state = A.state;
+  int b = rp[i], e = rp[i + 1];
+  int mine = 0;
+  for (int q = b + lane; q < e; q += 32) {
+    int j = ci[q];
+    if (j == i || !s[q]) continue;
+    int sj = state[j];
+    if (sj == CPT) {
+      mine += hash_insert(keys, mask, j);
+    } else if (sj == FPT) {
+      for (int q2 = rp[j]; q2 < rp[j + 1]; ++q2) {
+        int l = ci[q2];
+        if (l != j && s[q2] && state[l] == CPT) mine += hash_insert(keys, mask, l);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  __syncwarp();
+  return mine;
+}
+
 __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) {
   const int *rp = A.rp, *ci = A.ci;
   const double *v = A.v;
@@ -316,22 +342,7 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
   unsigned mask = (unsigned)T - 1;
   table_clear(t, T, lane);
   int b = rp[i], e = rp[i + 1];
-  int mine = 0;
-  for (int q = b + lane; q < e; q += 32) {
-    int j = ci[q];
-    if (j != i && s[q] && state[j] == CPT) mine += hash_insert(t.keys, mask, j);
-  }
-  for (int q = b + lane; q < e; q += 32) {
-    int k = ci[q];
-    if (k == i || !s[q] || state[k] != FPT) continue;
-    for (int q2 = rp[k]; q2 < rp[k + 1]; ++q2) {
-      int l = ci[q2];
-      if (l != k && s[q2] && state[l] == CPT) mine += hash_insert(t.keys, mask, l);
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  int u = mine;
-  __syncwarp();
+  int u = ext_candidates(i, t.keys, mask, lane, A);
   int outlen = (A.max_elmts > 0 && u > A.max_elmts) ? A.max_elmts : u;
   if (A.mode == 0) {
     if (lane == 0) A.cnt[i] = outlen;
@@ -518,6 +529,59 @@ int coarse_map(const int8_t *state, int n, DBuf<int> &cmap) {
   return nc;
 }
 
+// count pass: distinct interpolatory candidates u_i (keys-only tables, high
+// occupancy); cnt = output row length (1 for C rows, min(u, max_elmts) else)
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_ext_count(int nrows, const int *rows, ExtArgs A, int *ucnt) {
+  __shared__ int skeys[WPB][T];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int *keys = skeys[wid];
+  for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB) {
+    int i = rows[r];
+    if (A.state[i] == CPT) {
+      if (lane == 0) { A.cnt[i] = 1; ucnt[i] = 0; }
+      continue;
+    }
+    for (int q = lane; q < T; q += 32) keys[q] = -1;
+    __syncwarp();
+    int u = ext_candidates(i, keys, (unsigned)T - 1, lane, A);
+    if (lane == 0) {
+      ucnt[i] = u;
+      A.cnt[i] = (A.max_elmts > 0 && u > A.max_elmts) ? A.max_elmts : u;
+    }
+    __syncwarp();
+  }
+}
+__global__ void k_ext_count_g(int nrows, const int *rows, const int64_t *goff, const int *gsize,
+                              unsigned char *pool, ExtArgs A, int *ucnt) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= nrows) return;
+  int i = rows[wid];
+  if (A.state[i] == CPT) {
+    if (lane == 0) { A.cnt[i] = 1; ucnt[i] = 0; }
+    return;
+  }
+  int T = gsize[wid];
+  int *keys = (int *)(pool + goff[wid]);
+  for (int q = lane; q < T; q += 32) keys[q] = -1;
+  __syncwarp();
+  int u = ext_candidates(i, keys, (unsigned)T - 1, lane, A);
+  if (lane == 0) {
+    ucnt[i] = u;
+    A.cnt[i] = (A.max_elmts > 0 && u > A.max_elmts) ? A.max_elmts : u;
+  }
+}
+
+template <int T, int WPB>
+static void launch_ext_count(int nrows, const int *rows, const ExtArgs &A, int *ucnt) {
+  if (!nrows) return;
+  int grid = (nrows + WPB - 1) / WPB;
+  int cap = g_ctx->num_sms * 32;
+  if (grid > cap) grid = cap;
+  k_ext_count<T, WPB><<<grid, WPB * 32, 0, stream()>>>(nrows, rows, A, ucnt);
+  check_launch("ext_count");
+}
+
 Csr ext_interp(const Csr &a, const int8_t *s, const int8_t *state, const int *cmap, int nc, int max_elmts) {
   int n = a.nr;
   Csr p;
@@ -525,16 +589,33 @@ Csr ext_interp(const Csr &a, const int8_t *s, const int8_t *state, const int *cm
   p.nc = nc;
   p.b = 1;
   p.rp.alloc((size_t)n + 1);
-  DBuf<int> ub((size_t)(n ? n : 1)), cnt((size_t)(n ? n : 1)), bad(1);
+  DBuf<int> ub((size_t)(n ? n : 1)), cnt((size_t)(n ? n : 1)), ucnt((size_t)(n ? n : 1)), bad(1);
   int big = 0x7fffffff;
   h2d(bad.p, &big, sizeof(int));
   if (n) {
     k_ext_ub<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, state, ub.p);
     check_launch("ext_ub");
   }
-  RowBins bins;
-  bins.build(ub.p, n);
   ExtArgs A{a.rp.p, a.ci.p, a.v.p, s, state, cmap, max_elmts, 0, cnt.p, nullptr, nullptr, nullptr, bad.p};
+  {
+    RowBins cb;
+    cb.build(ub.p, n, 1);
+    launch_ext_count<64, 8>(cb.cnt[0], cb.rows.p + cb.off[0], A, ucnt.p);
+    launch_ext_count<128, 8>(cb.cnt[1], cb.rows.p + cb.off[1], A, ucnt.p);
+    launch_ext_count<256, 8>(cb.cnt[2], cb.rows.p + cb.off[2], A, ucnt.p);
+    launch_ext_count<512, 8>(cb.cnt[3], cb.rows.p + cb.off[3], A, ucnt.p);
+    launch_ext_count<1024, 8>(cb.cnt[4], cb.rows.p + cb.off[4], A, ucnt.p);
+    launch_ext_count<2048, 4>(cb.cnt[5], cb.rows.p + cb.off[5], A, ucnt.p);
+    launch_ext_count<4096, 2>(cb.cnt[6], cb.rows.p + cb.off[6], A, ucnt.p);
+    int ng = cb.cnt[NBIN];
+    if (ng) {
+      k_ext_count_g<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(ng, cb.rows.p + cb.off[NBIN], cb.goff.p,
+                                                                            cb.gsize.p, cb.pool.p, A, ucnt.p);
+      check_launch("ext_count_g");
+    }
+  }
+  RowBins bins;
+  bins.build(ucnt.p, n, 0);
   auto run = [&]() {
     launch_ext<64, 8>(bins.cnt[0], bins.rows.p + bins.off[0], A);
     launch_ext<128, 8>(bins.cnt[1], bins.rows.p + bins.off[1], A);
@@ -551,7 +632,6 @@ Csr ext_interp(const Csr &a, const int8_t *s, const int8_t *state, const int *cm
       check_launch("ext_gmem");
     }
   };
-  run();
   p.nnz = exclusive_scan_i32_to_i32(cnt.p, p.rp.p, n);
   p.ci.alloc((size_t)p.nnz);
   p.v.alloc((size_t)p.nnz);

@@ -142,7 +142,9 @@ struct RowBins {
   DBuf<int> gsize;         // global bin: table slots per row
   DBuf<int64_t> goff;      // global bin: byte offsets into pool
   DBuf<unsigned char> pool;
-  void build(const int *ub_dev, int m, bool staged_global = false);
+  // layout of the global tables: 0 = WarpTables (14T), 1 = keys only (4T),
+  // 2 = SpGEMM fill tables (14T + 256)
+  void build(const int *ub_dev, int m, int layout = 0);
 };
 
 }  // namespace mg

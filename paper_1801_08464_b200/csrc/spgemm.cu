@@ -2,15 +2,20 @@
 // submatrix extraction.
 //
 // SpGEMM (replaces scipy csr_matmat at triple_product, sparse.py:199-203 —
-// MGR RAP mgr.py:288 and AMG Galerkin amg.py:318):
-// Gustavson row-by-row, one warp per output row, shared-memory hash tables
-// sized by the row's product upper bound (bins of 256 / 1024 / 4096 slots, a
-// global-memory table beyond).  Bit-exact with scipy:
-// each output column accumulates 0 + a_ij1*b_j1k + a_ij2*b_j2k + ... with j
-// in the left row's stored (ascending) order, a separate multiply and add
-// (libmgrgpu is built with --fmad=false), exact zeros dropped, columns sorted.
-// The lanes of the warp split the entries of B_j (distinct columns, so no
-// two lanes touch one accumulator) and step through j in order.
+// MGR RAP mgr.py:288 and AMG Galerkin amg.py:318).
+// Gustavson row by row, one warp per output row, two passes:
+//   count: distinct columns per row (hash of keys only, table >= 2x the
+//          row's product count), sizes the output;
+//   fill:  table sized by the exact distinct count (>= 2x), accumulators per
+//          hash slot, then the keys are sorted and written with their sums.
+// Products are generated in windows of 32: a warp scan of |B_j| over 32
+// entries of A's row and a per-lane binary search map window lane -> (j, k),
+// so every lane issues its global loads at once.  Bit-exact with scipy
+// (SURVEY.md §8(c) p2): each output column is accumulated as
+// 0 + a_ij1*b_j1k + a_ij2*b_j2k + ... in (j, k) stored order with a separate
+// multiply and add — within a window, lanes hitting the same column are
+// serialised in lane order by __match_any_sync groups — and exact zeros are
+// dropped after the product, columns sorted.
 #include "ops.cuh"
 #include "sparse_util.cuh"
 #include "hash.cuh"
@@ -18,131 +23,213 @@
 
 namespace mg {
 
-// One output row.  mode 0: count unique columns -> cnt[row].
-// mode 1: fill sorted (col, val) at out + base, nonzero count -> nz[row].
-static __device__ void spgemm_row(int row, int T, WarpTables t, int lane, const int *__restrict__ arp,
-                                  const int *__restrict__ aci, const double *__restrict__ av,
-                                  const int *__restrict__ brp, const int *__restrict__ bci,
-                                  const double *__restrict__ bv, int mode, int *cnt,
-                                  const int64_t *base, int *oci, double *ov, int *nz) {
-  unsigned mask = (unsigned)T - 1;
-  table_clear(t, T, lane);
+// insert and return the slot; *fresh = 1 when this lane created it
+__device__ __forceinline__ int hash_insert_slot(int *keys, unsigned mask, int k, int *fresh) {
+  unsigned h = hash_k(k, mask);
+  while (true) {
+    int cur = keys[h];
+    if (cur == k) { *fresh = 0; return (int)h; }
+    if (cur == -1) {
+      int old = atomicCAS(&keys[h], -1, k);
+      if (old == -1) { *fresh = 1; return (int)h; }
+      if (old == k) { *fresh = 0; return (int)h; }
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// Walk the products of A row `row` (j ascending, B_j stored order) in windows
+// of 32; calls f(valid, k, prod) with all lanes converged, in product order.
+template <bool NEED_VAL, class F>
+__device__ __forceinline__ void for_products(int row, int lane, const int *__restrict__ arp,
+                                             const int *__restrict__ aci, const double *__restrict__ av,
+                                             const int *__restrict__ brp, const int *__restrict__ bci,
+                                             const double *__restrict__ bv, F &&f) {
   int s = arp[row], e = arp[row + 1];
-  int mine = 0;
-  if (mode == 0) {
-    for (int q = s + lane; q < e; q += 32) {
-      int j = aci[q];
-      for (int r = brp[j]; r < brp[j + 1]; ++r) mine += hash_insert(t.keys, mask, bci[r]);
-    }
-    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
-    if (lane == 0) cnt[row] = mine;
-    return;
-  }
-  if (!t.pcol) {
-    // large rows: no staging buffer; j ascending, lanes over B_j
-    for (int q = s + lane; q < e; q += 32) {
-      int j = aci[q];
-      for (int r = brp[j]; r < brp[j + 1]; ++r) mine += hash_insert(t.keys, mask, bci[r]);
-    }
-    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
-    int u = mine;
-    __syncwarp();
-    table_sort(t, T, u, lane);
-    for (int q = lane; q < u; q += 32) t.acc[q] = 0.0;
-    __syncwarp();
-    for (int q = s; q < e; ++q) {
-      int j = aci[q];
-      double a = av[q];
-      for (int r = brp[j] + lane; r < brp[j + 1]; r += 32) {
-        int p = t.pos[hash_find(t.keys, mask, bci[r])];
-        t.acc[p] = __dadd_rn(t.acc[p], __dmul_rn(a, bv[r]));
-      }
-      __syncwarp();
-    }
-    int64_t o = base[row];
-    int nzc = 0;
-    for (int q = lane; q < u; q += 32) {
-      oci[o + q] = t.list[q];
-      double val = t.acc[q];
-      ov[o + q] = val;
-      nzc += val != 0.0;
-    }
-    for (int off = 16; off > 0; off >>= 1) nzc += __shfl_xor_sync(0xffffffffu, nzc, off);
-    if (lane == 0) nz[row] = nzc;
-    return;
-  }
-  // stage every product a_ij*b_jk in (j, k) stored order: lanes own consecutive
-  // entries of A's row, a warp scan of |B_j| gives each lane its output offset
-  int np = 0;
   for (int q0 = s; q0 < e; q0 += 32) {
     int q = q0 + lane;
-    int j = 0, rb = 0, re = 0;
+    int rb = 0, len = 0;
     double a = 0.0;
     if (q < e) {
-      j = aci[q];
-      a = av[q];
-      rb = brp[j];
-      re = brp[j + 1];
+      int j = __ldg(aci + q);
+      if (NEED_VAL) a = __ldg(av + q);
+      rb = __ldg(brp + j);
+      len = __ldg(brp + j + 1) - rb;
     }
-    int len = re - rb, incl = len;
+    int incl = len;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, incl, off);
       if (lane >= off) incl += y;
     }
-    int o = np + incl - len;
-    for (int r = rb; r < re; ++r, ++o) {
-      int k = bci[r];
-      t.pcol[o] = k;
-      t.pval[o] = __dmul_rn(a, bv[r]);
-      mine += hash_insert(t.keys, mask, k);
+    int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int w0 = 0; w0 < total; w0 += 32) {
+      int p = w0 + lane;
+      // src = first lane with incl > p
+      int lo = 0, hi = 31;
+#pragma unroll
+      for (int it = 0; it < 5; ++it) {
+        int mid = (lo + hi) >> 1;
+        int v = __shfl_sync(0xffffffffu, incl, mid);
+        if (p < v) hi = mid; else lo = mid + 1;
+      }
+      int src = lo;
+      int s_incl = __shfl_sync(0xffffffffu, incl, src);
+      int s_len = __shfl_sync(0xffffffffu, len, src);
+      int s_rb = __shfl_sync(0xffffffffu, rb, src);
+      double s_a = NEED_VAL ? __shfl_sync(0xffffffffu, a, src) : 0.0;
+      bool valid = p < total;
+      int k = -1;
+      double prod = 0.0;
+      if (valid) {
+        int r = s_rb + (p - (s_incl - s_len));
+        k = __ldg(bci + r);
+        if (NEED_VAL) prod = __dmul_rn(s_a, __ldg(bv + r));
+      }
+      f(valid, k, prod);
     }
-    np += __shfl_sync(0xffffffffu, incl, 31);
   }
+}
+
+// ---- count pass: keys only ------------------------------------------------------
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_spgemm_count(int nrows, const int *rows, const int *arp,
+                                                           const int *aci, const int *brp, const int *bci,
+                                                           int *cnt) {
+  __shared__ int skeys[WPB][T];
+  int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int *keys = skeys[wid];
+  const unsigned mask = T - 1;
+  for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB) {
+    int row = rows[r];
+    for (int i = lane; i < T; i += 32) keys[i] = -1;
+    __syncwarp();
+    int mine = 0;
+    for_products<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, [&](bool valid, int k, double) {
+      if (valid) mine += hash_insert(keys, mask, k);
+    });
+    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+    if (lane == 0) cnt[row] = mine;
+    __syncwarp();
+  }
+}
+
+// global-memory keys for rows beyond the largest smem bin
+__global__ void k_spgemm_count_g(int nrows, const int *rows, const int64_t *goff, const int *gsize,
+                                 unsigned char *pool, const int *arp, const int *aci, const int *brp,
+                                 const int *bci, int *cnt) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= nrows) return;
+  int T = gsize[wid];
+  int *keys = (int *)(pool + goff[wid]);
+  unsigned mask = (unsigned)T - 1;
+  int row = rows[wid];
+  for (int i = lane; i < T; i += 32) keys[i] = -1;
+  __syncwarp();
+  int mine = 0;
+  for_products<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, [&](bool valid, int k, double) {
+    if (valid) mine += hash_insert(keys, mask, k);
+  });
   for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
-  int u = mine;
+  if (lane == 0) cnt[row] = mine;
+}
+
+// ---- fill pass ------------------------------------------------------------------
+struct FillTabs {
+  int *keys;     // T
+  double *acc;   // T (per slot)
+  int *list;     // T/2 (sorted keys)
+  double *win;   // 32 window values
+};
+
+__device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, const int *arp, const int *aci,
+                                         const double *av, const int *brp, const int *bci, const double *bv,
+                                         const int64_t *base, int *oci, double *ov, int *nz) {
+  const unsigned mask = (unsigned)T - 1;
+  for (int i = lane; i < T; i += 32) t.keys[i] = -1;
   __syncwarp();
-  table_sort(t, T, u, lane);
-  for (int q = lane; q < u; q += 32) t.acc[q] = 0.0;
+  int u = 0;
+  for_products<true>(row, lane, arp, aci, av, brp, bci, bv, [&](bool valid, int k, double prod) {
+    int fresh = 0;
+    int slot = valid ? hash_insert_slot(t.keys, mask, k, &fresh) : -1 - lane;
+    if (fresh) t.acc[slot] = 0.0;
+    t.win[lane] = prod;
+    u += __popc(__ballot_sync(0xffffffffu, fresh));
+    unsigned grp = __match_any_sync(0xffffffffu, slot);
+    __syncwarp();
+    if (valid && lane == __ffs(grp) - 1) {
+      double sacc = t.acc[slot];
+      unsigned m = grp;
+      while (m) {
+        int l = __ffs(m) - 1;
+        sacc = __dadd_rn(sacc, t.win[l]);
+        m &= m - 1;
+      }
+      t.acc[slot] = sacc;
+    }
+    __syncwarp();
+  });
+  // sorted key list
+  int P = 32;
+  while (P < u) P <<= 1;
+  int filled = 0;
+  for (int i0 = 0; i0 < T; i0 += 32) {
+    int k = t.keys[i0 + lane];
+    unsigned bal = __ballot_sync(0xffffffffu, k != -1);
+    if (k != -1) t.list[filled + __popc(bal & ((1u << lane) - 1))] = k;
+    filled += __popc(bal);
+  }
+  for (int i = u + lane; i < P; i += 32) t.list[i] = 0x7fffffff;
   __syncwarp();
-  // ordered accumulation: 0 + p_1 + p_2 + ... in staged (= scipy) order per column
-  ordered_accumulate(t, mask, np, lane);
+  warp_bitonic(t.list, P, lane);
   int64_t o = base[row];
   int nzc = 0;
   for (int q = lane; q < u; q += 32) {
-    oci[o + q] = t.list[q];
-    double val = t.acc[q];
+    int k = t.list[q];
+    double val = t.acc[hash_find(t.keys, mask, k)];
+    oci[o + q] = k;
     ov[o + q] = val;
     nzc += val != 0.0;
   }
   for (int off = 16; off > 0; off >>= 1) nzc += __shfl_xor_sync(0xffffffffu, nzc, off);
   if (lane == 0) nz[row] = nzc;
+  __syncwarp();
 }
 
-template <int T, int WPB, bool STAGED>
-__global__ void __launch_bounds__(WPB * 32) k_spgemm_smem(int nrows, const int *rows, const int *arp,
-                                                          const int *aci, const double *av,
-                                                          const int *brp, const int *bci,
-                                                          const double *bv, int mode, int *cnt,
-                                                          const int64_t *base, int *oci, double *ov,
-                                                          int *nz) {
+template <int T>
+__host__ __device__ constexpr size_t fill_bytes() { return (size_t)T * 4 + (size_t)T * 8 + (size_t)T * 2 + 256; }
+
+template <int T, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_spgemm_fill(int nrows, const int *rows, const int *arp,
+                                                          const int *aci, const double *av, const int *brp,
+                                                          const int *bci, const double *bv, const int64_t *base,
+                                                          int *oci, double *ov, int *nz) {
   extern __shared__ __align__(16) unsigned char smem[];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpTables t = carve(smem + table_bytes(T, STAGED) * wid, T, STAGED);
+  unsigned char *w = smem + fill_bytes<T>() * wid;
+  FillTabs t;
+  t.acc = (double *)w;
+  t.win = t.acc + T;
+  t.keys = (int *)(t.win + 32);
+  t.list = t.keys + T;
   for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB)
-    spgemm_row(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, mode, cnt, base, oci, ov, nz);
+    fill_row(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
 }
 
-// global-memory tables for rows with huge product bounds (one warp per row)
-__global__ void k_spgemm_gmem(int nrows, const int *rows, const int64_t *tab_off, const int *tab_size,
-                              unsigned char *pool, const int *arp, const int *aci, const double *av,
-                              const int *brp, const int *bci, const double *bv, int mode, int *cnt,
-                              const int64_t *base, int *oci, double *ov, int *nz) {
+__global__ void k_spgemm_fill_g(int nrows, const int *rows, const int64_t *goff, const int *gsize,
+                                unsigned char *pool, const int *arp, const int *aci, const double *av,
+                                const int *brp, const int *bci, const double *bv, const int64_t *base, int *oci,
+                                double *ov, int *nz) {
   int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= nrows) return;
-  int T = tab_size[wid];
-  WarpTables t = carve(pool + tab_off[wid], T, false);
-  spgemm_row(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, mode, cnt, base, oci, ov, nz);
+  int T = gsize[wid];
+  unsigned char *w = pool + goff[wid];
+  FillTabs t;
+  t.acc = (double *)w;
+  t.win = t.acc + T;
+  t.keys = (int *)(t.win + 32);
+  t.list = t.keys + T;
+  fill_row(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
 }
 
 // compaction: drop exact zeros, keep order (warp per row)
@@ -195,7 +282,6 @@ __global__ void k_bin_count(int m, const int *ub, int *bin_cnt) {
   __syncthreads();
   if (threadIdx.x <= NBIN && h[threadIdx.x]) atomicAdd(&bin_cnt[threadIdx.x], h[threadIdx.x]);
 }
-// stable within a block: block-local ranks, one global reservation per bin per block
 __global__ void k_bin_fill(int m, const int *ub, int *fillpos, int *rows) {
   __shared__ int h[NBIN + 1], base[NBIN + 1];
   if (threadIdx.x <= NBIN) h[threadIdx.x] = 0;
@@ -211,14 +297,16 @@ __global__ void k_bin_fill(int m, const int *ub, int *fillpos, int *rows) {
   __syncthreads();
   if (b >= 0) rows[base[b] + r] = i;
 }
-__global__ void k_gmem_tabs(int nr, const int *rows, const int *ub, int *tsz, int *units, int staged) {
+// global tables: T = pow2 >= 2 ub, bytes from the requested layout
+__global__ void k_gmem_tabs(int nr, const int *rows, const int *ub, int *tsz, int *units, int layout) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nr) return;
   int u = ub[rows[i]];
   int T = 64;
   while (T < 2 * u) T <<= 1;
   tsz[i] = T;
-  units[i] = (int)((table_bytes(T, staged != 0) + 15) / 16);  // 16-byte units
+  size_t bytes = layout == 0 ? table_bytes(T, false) : layout == 1 ? (size_t)T * 4 : (size_t)T * 14 + 256;
+  units[i] = (int)((bytes + 15) / 16);  // 16-byte units
 }
 
 __global__ void k_scale_i64(int64_t *a, int64_t s, int n) {
@@ -230,7 +318,7 @@ void scale_i64(int64_t *a, int64_t s, int n) {
   check_launch("scale_i64");
 }
 
-void RowBins::build(const int *ub_dev, int m, bool staged_global) {
+void RowBins::build(const int *ub_dev, int m, int layout) {
   DBuf<int> bc(NBIN + 1);
   dzero(bc.p, sizeof(int) * (NBIN + 1));
   if (m) {
@@ -251,8 +339,7 @@ void RowBins::build(const int *ub_dev, int m, bool staged_global) {
     gsize.alloc(ng);
     DBuf<int> units(ng);
     goff.alloc((size_t)ng + 1);
-    k_gmem_tabs<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, rows.p + off[NBIN], ub_dev, gsize.p, units.p,
-                                                          staged_global ? 1 : 0);
+    k_gmem_tabs<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, rows.p + off[NBIN], ub_dev, gsize.p, units.p, layout);
     check_launch("gmem_tabs");
     int64_t tot = exclusive_scan_i32_to_i64(units.p, goff.p, ng);
     pool.alloc((size_t)tot * 16);
@@ -260,19 +347,29 @@ void RowBins::build(const int *ub_dev, int m, bool staged_global) {
   }
 }
 
-template <int T, int WPB, bool STAGED>
-static void launch_bin(int nrows, const int *rows, const Csr &a, const Csr &b, int mode, int *cnt,
-                       const int64_t *base, int *oci, double *ov, int *nz) {
+static int cap_grid(int nrows, int wpb) {
+  int grid = (nrows + wpb - 1) / wpb;
+  int cap = g_ctx->num_sms * 32;
+  return grid > cap ? cap : grid;
+}
+
+template <int T, int WPB>
+static void launch_count(int nrows, const int *rows, const Csr &a, const Csr &b, int *cnt) {
   if (!nrows) return;
-  size_t sm = table_bytes(T, STAGED) * WPB;
-  MG_CUDA(cudaFuncSetAttribute(k_spgemm_smem<T, WPB, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sm));
-  int grid = (nrows + WPB - 1) / WPB;
-  int cap = g_ctx->num_sms * 16;
-  if (grid > cap) grid = cap;
-  k_spgemm_smem<T, WPB, STAGED><<<grid, WPB * 32, sm, stream()>>>(nrows, rows, a.rp.p, a.ci.p, a.v.p, b.rp.p,
-                                                                  b.ci.p, b.v.p, mode, cnt, base, oci, ov, nz);
-  check_launch("spgemm_smem");
+  k_spgemm_count<T, WPB><<<cap_grid(nrows, WPB), WPB * 32, 0, stream()>>>(nrows, rows, a.rp.p, a.ci.p, b.rp.p,
+                                                                          b.ci.p, cnt);
+  check_launch("spgemm_count");
+}
+
+template <int T, int WPB>
+static void launch_fill(int nrows, const int *rows, const Csr &a, const Csr &b, const int64_t *base, int *oci,
+                        double *ov, int *nz) {
+  if (!nrows) return;
+  size_t sm = fill_bytes<T>() * WPB;
+  MG_CUDA(cudaFuncSetAttribute(k_spgemm_fill<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_spgemm_fill<T, WPB><<<cap_grid(nrows, WPB), WPB * 32, sm, stream()>>>(nrows, rows, a.rp.p, a.ci.p, a.v.p,
+                                                                          b.rp.p, b.ci.p, b.v.p, base, oci, ov, nz);
+  check_launch("spgemm_fill");
 }
 
 Csr spgemm(const Csr &a, const Csr &b) {
@@ -288,33 +385,52 @@ Csr spgemm(const Csr &a, const Csr &b) {
   DBuf<int> ub(m), cnt(m), nz(m);
   k_row_ub<<<grid_for((int64_t)m * 32, 256), 256, 0, stream()>>>(m, a.rp.p, a.ci.p, b.rp.p, ub.p);
   check_launch("row_ub");
-  RowBins bins;
-  bins.build(ub.p, m);
-  auto run = [&](int mode, const int64_t *base, int *oci, double *ov) {
-#define BIN(k, T, W, S) \
-    launch_bin<T, W, S>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, mode, cnt.p, base, oci, ov, nz.p)
-    BIN(0, 64, 8, true);
-    BIN(1, 128, 8, true);
-    BIN(2, 256, 8, true);
-    BIN(3, 512, 8, true);
-    BIN(4, 1024, 4, true);
-    BIN(5, 2048, 2, true);
-    BIN(6, 4096, 2, false);
-#undef BIN
+  {
+    // count pass, tables sized by the product count (all keys could be distinct)
+    RowBins bins;
+    bins.build(ub.p, m, 1);
+#define CB(k, T, W) launch_count<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, cnt.p)
+    CB(0, 64, 8);
+    CB(1, 128, 8);
+    CB(2, 256, 8);
+    CB(3, 512, 8);
+    CB(4, 1024, 8);
+    CB(5, 2048, 4);
+    CB(6, 4096, 2);
+#undef CB
     int ng = bins.cnt[NBIN];
     if (ng) {
-      k_spgemm_gmem<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
-          ng, bins.rows.p + bins.off[NBIN], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, a.v.p,
-          b.rp.p, b.ci.p, b.v.p, mode, cnt.p, base, oci, ov, nz.p);
-      check_launch("spgemm_gmem");
+      k_spgemm_count_g<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
+          ng, bins.rows.p + bins.off[NBIN], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, b.rp.p, b.ci.p,
+          cnt.p);
+      check_launch("spgemm_count_g");
     }
-  };
-  run(0, nullptr, nullptr, nullptr);
+  }
   DBuf<int64_t> trp((size_t)m + 1);
   int64_t total = exclusive_scan_i32_to_i64(cnt.p, trp.p, m);
   DBuf<int> tci((size_t)total);
   DBuf<double> tv((size_t)total);
-  run(1, trp.p, tci.p, tv.p);
+  {
+    // fill pass, tables sized by the exact distinct count
+    RowBins bins;
+    bins.build(cnt.p, m, 2);
+#define FB(k, T, W) launch_fill<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, trp.p, tci.p, tv.p, nz.p)
+    FB(0, 64, 8);
+    FB(1, 128, 8);
+    FB(2, 256, 8);
+    FB(3, 512, 8);
+    FB(4, 1024, 8);
+    FB(5, 2048, 4);
+    FB(6, 4096, 2);
+#undef FB
+    int ng = bins.cnt[NBIN];
+    if (ng) {
+      k_spgemm_fill_g<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
+          ng, bins.rows.p + bins.off[NBIN], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, a.v.p, b.rp.p,
+          b.ci.p, b.v.p, trp.p, tci.p, tv.p, nz.p);
+      check_launch("spgemm_fill_g");
+    }
+  }
   c.nr = m;
   c.nc = b.nc;
   c.b = 1;
@@ -327,8 +443,7 @@ Csr spgemm(const Csr &a, const Csr &b) {
   } else {
     c.ci.alloc((size_t)kept);
     c.v.alloc((size_t)kept);
-    k_compact<<<grid_for((int64_t)m * 32, 256), 256, 0, stream()>>>(m, trp.p, tci.p, tv.p, c.rp.p, c.ci.p,
-                                                                     c.v.p);
+    k_compact<<<grid_for((int64_t)m * 32, 256), 256, 0, stream()>>>(m, trp.p, tci.p, tv.p, c.rp.p, c.ci.p, c.v.p);
     check_launch("compact");
   }
   return c;
