@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <map>
+#include <memory>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -99,16 +100,29 @@ struct DBuf {
   T *get() const { return p; }
 };
 
+// SpMV launch plan of a scalar CSR: rows binned by length class so bimodal
+// matrices (identity rows of gas-absent cells next to ~60-entry Schur rows)
+// get a lane-group size per class (spmv.cu prepare_spmv).
+struct SpmvPlan {
+  static const int NC = 7;
+  bool binned = false;
+  int single = 0;            // class used when not binned
+  int cnt[NC] = {}, off[NC] = {};
+  DBuf<int> rows;            // row lists grouped by class
+};
+
 // Device CSR; b > 1 means block CSR with b*b row-major values per entry.
 struct Csr {
   int nr = 0, nc = 0, b = 1;
   int64_t nnz = 0;
   DBuf<int> rp, ci;
   DBuf<double> v;
+  mutable std::unique_ptr<SpmvPlan> plan;
   Csr() = default;
   Csr(Csr &&) = default;
   Csr &operator=(Csr &&) = default;
   void alloc(int nr_, int nc_, int64_t nnz_, int b_ = 1) {
+    plan.reset();
     nr = nr_; nc = nc_; nnz = nnz_; b = b_;
     rp.alloc((size_t)nr + 1);
     ci.alloc((size_t)nnz);

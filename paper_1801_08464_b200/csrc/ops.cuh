@@ -5,6 +5,8 @@
 namespace mg {
 
 // ---- SpMV family (spmv.cu) --------------------------------------------------
+// bin rows by length class once (syncs); done at setup for solve-phase matrices
+void prepare_spmv(const Csr &a);
 // y = A x
 void spmv(const Csr &a, const double *x, double *y);
 // r = b - A x

@@ -123,6 +123,9 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
     if (l + 1 < h->L.size()) {
       v.l1inv.alloc(n);
       l1_inverse(v.A, v.l1inv.p);
+      prepare_spmv(v.A);
+      prepare_spmv(v.P);
+      prepare_spmv(v.R);
     }
   }
   AmgLevel &last = h->L.back();
@@ -387,6 +390,10 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       for (int c = 0; c < lv.nc; ++c) nxt_cells[c] = cells[cl[c]];
     }
     cells.swap(nxt_cells);
+    prepare_spmv(cur);
+    prepare_spmv(lv.R);
+    prepare_spmv(lv.P);
+    prepare_spmv(lv.Aff);
     lv.res.alloc(n);
     lv.rF.alloc(lv.nf);
     lv.eF.alloc(lv.nf);

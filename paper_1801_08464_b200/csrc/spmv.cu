@@ -34,7 +34,8 @@ struct EpiJacobi {
 // matrix traffic outstanding per round trip.  Groups stride over rows (grid
 // sized to the resident capacity); every lane runs the shuffle (uniform loop).
 template <int VS, int U, class Epi>
-__global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ rp,
+__global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ rows,
+                                             const int *__restrict__ rp,
                                              const int *__restrict__ ci,
                                              const double *__restrict__ v,
                                              const double *__restrict__ x, Epi epi) {
@@ -42,9 +43,10 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ rp,
   const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VS);
   const int ng = (int)((int64_t)gridDim.x * blockDim.x / VS);
   const int warp_first = (int)(((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / VS);
-  for (int row = g0, wf = warp_first; wf < nr; row += ng, wf += ng) {
+  for (int idx = g0, wf = warp_first; wf < nr; idx += ng, wf += ng) {
     double sum = 0.0;
-    if (row < nr) {
+    int row = idx < nr ? (rows ? __ldg(rows + idx) : idx) : nr;
+    if (idx < nr) {
       int s = __ldg(rp + row), e = __ldg(rp + row + 1);
       for (int k0 = s; k0 < e; k0 += VS * U) {
         double vv[U];
@@ -63,8 +65,67 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ rp,
     }
 #pragma unroll
     for (int off = VS / 2; off > 0; off >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, off, VS);
-    if (row < nr && lane == 0) epi(row, sum);
+    if (idx < nr && lane == 0) epi(row, sum);
   }
+}
+
+// ---- SpMV plan: rows binned by length class ---------------------------------------
+// class c: len <= 2, 6, 12, 24, 48, 96, >96  ->  (VS, U) below
+__device__ __forceinline__ int len_class(int len) {
+  return len <= 2 ? 0 : len <= 6 ? 1 : len <= 12 ? 2 : len <= 24 ? 3 : len <= 48 ? 4 : len <= 96 ? 5 : 6;
+}
+__global__ void k_cls_count(int n, const int *rp, int *cnt) {
+  __shared__ int h[SpmvPlan::NC];
+  if (threadIdx.x < SpmvPlan::NC) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[len_class(rp[i + 1] - rp[i])], 1);
+  __syncthreads();
+  if (threadIdx.x < SpmvPlan::NC && h[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], h[threadIdx.x]);
+}
+__global__ void k_cls_fill(int n, const int *rp, int *fill, int *rows) {
+  __shared__ int h[SpmvPlan::NC], base[SpmvPlan::NC];
+  if (threadIdx.x < SpmvPlan::NC) h[threadIdx.x] = 0;
+  __syncthreads();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int c = -1, r = 0;
+  if (i < n) {
+    c = len_class(rp[i + 1] - rp[i]);
+    r = atomicAdd(&h[c], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < SpmvPlan::NC && h[threadIdx.x]) base[threadIdx.x] = atomicAdd(&fill[threadIdx.x], h[threadIdx.x]);
+  __syncthreads();
+  if (c >= 0) rows[base[c] + r] = i;
+}
+
+void prepare_spmv(const Csr &a) {
+  if (a.plan || a.b != 1) return;
+  auto pl = std::make_unique<SpmvPlan>();
+  const int NC = SpmvPlan::NC;
+  if (a.nr > 0) {
+    DBuf<int> cnt(NC);
+    dzero(cnt.p, sizeof(int) * NC);
+    k_cls_count<<<grid_for(a.nr, 256, g_ctx->num_sms * 4), 256, 0, stream()>>>(a.nr, a.rp.p, cnt.p);
+    check_launch("cls_count");
+    d2h(pl->cnt, cnt.p, sizeof(int) * NC);
+    int best = 0;
+    for (int c = 1; c < NC; ++c)
+      if (pl->cnt[c] > pl->cnt[best]) best = c;
+    pl->single = best;
+    // per-class binning is kept for experiments but off: measured slower on the
+    // config-3 hierarchy (row-list indirection = one more dependent load per row)
+    const bool enable_binning = false;
+    if (enable_binning && a.nr >= 4096 && pl->cnt[best] < 0.92 * a.nr) {
+      pl->binned = true;
+      for (int c = 1; c < NC; ++c) pl->off[c] = pl->off[c - 1] + pl->cnt[c - 1];
+      h2d(cnt.p, pl->off, sizeof(int) * NC);
+      pl->rows.alloc(a.nr);
+      k_cls_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, cnt.p, pl->rows.p);
+      check_launch("cls_fill");
+    }
+  }
+  a.plan = std::move(pl);
 }
 
 template <int B, int G, int U>
@@ -151,18 +212,40 @@ static void launch_csr(const Csr &a, const double *x, Epi epi) {
   const int T = 256;
   cudaStream_t s = stream();
   (void)T;
-#define LAUNCH(VS, U)                                                               \
-  k_csr<VS, U, Epi><<<spmv_grid((int64_t)a.nr * VS), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, \
-                                                                  a.v.p, x, epi)
-  if (avg <= 2.5) LAUNCH(2, 2);
-  else if (avg <= 5) LAUNCH(4, 2);
-  else if (avg <= 9) LAUNCH(4, 3);
-  else if (avg <= 18) LAUNCH(8, 3);
-  else if (avg <= 36) LAUNCH(16, 3);
-  else if (avg <= 72) LAUNCH(16, 5);
-  else LAUNCH(32, 4);
+#define LAUNCH_AVG(VS, U) \
+  k_csr<VS, U, Epi><<<spmv_grid((int64_t)a.nr * VS), 256, 0, s>>>(a.nr, nullptr, a.rp.p, a.ci.p, a.v.p, x, epi)
+  prepare_spmv(a);
+  const SpmvPlan &pl = *a.plan;
+  auto run = [&](int c, int n, const int *rows) {
+    if (!n) return;
+#define LAUNCH(VS, U) \
+  k_csr<VS, U, Epi><<<spmv_grid((int64_t)n * VS), 256, 0, s>>>(n, rows, a.rp.p, a.ci.p, a.v.p, x, epi)
+    switch (c) {
+      case 0: LAUNCH(1, 2); break;
+      case 1: LAUNCH(2, 3); break;
+      case 2: LAUNCH(4, 3); break;
+      case 3: LAUNCH(8, 3); break;
+      case 4: LAUNCH(16, 3); break;
+      case 5: LAUNCH(32, 3); break;
+      default: LAUNCH(32, 4); break;
+    }
 #undef LAUNCH
-  check_launch("csr spmv");
+    check_launch("csr spmv");
+  };
+  if (!pl.binned) {
+    // lane-group size from the average row length (measured better than
+    // per-class binning: the row-list indirection adds a dependent load)
+    if (avg <= 2.5) LAUNCH_AVG(2, 2);
+    else if (avg <= 5) LAUNCH_AVG(4, 2);
+    else if (avg <= 9) LAUNCH_AVG(4, 3);
+    else if (avg <= 18) LAUNCH_AVG(8, 3);
+    else if (avg <= 36) LAUNCH_AVG(16, 3);
+    else if (avg <= 72) LAUNCH_AVG(16, 5);
+    else LAUNCH_AVG(32, 4);
+    check_launch("csr spmv");
+    return;
+  }
+  for (int c = 0; c < SpmvPlan::NC; ++c) run(c, pl.cnt[c], pl.rows.p + pl.off[c]);
 }
 
 void spmv(const Csr &a, const double *x, double *y) {
