@@ -109,6 +109,14 @@ struct SpmvPlan {
   int single = 0;            // class used when not binned
   int cnt[NC] = {}, off[NC] = {};
   DBuf<int> rows;            // row lists grouped by class
+  // SELL-32 copy (slices of 32 consecutive rows, column-major inside a slice):
+  // one thread per row, coalesced value/column loads and x gathers that
+  // coalesce across neighbouring stencil rows.  Built when padding <= 15%.
+  bool sell = false;
+  DBuf<int> sptr;            // slice start (elements), nslices + 1
+  DBuf<int> rlen;            // row lengths
+  DBuf<int> sci;
+  DBuf<double> sv;
 };
 
 // Device CSR; b > 1 means block CSR with b*b row-major values per entry.

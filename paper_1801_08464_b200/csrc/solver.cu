@@ -52,15 +52,22 @@ void prof_collect() {
 
 // ================================ AMG ==============================================
 double Amg::cycle_bytes() const {
-  // sum_l (pre+post) (SpMV_l + 24 n_l) + SpMV_l + SpMV(R_l) + SpMV(P_l) + 16 n_l
+  // Algorithmic bytes of one V(pre, post) cycle from x = 0, as executed
+  // (SURVEY.md §8(d) with the zero-guess first sweep counted as what it is):
+  //   first pre-sweep  x = D^-1 b            24 n
+  //   each further sweep (SpMV_l + 16 n)     (reads b, D^-1; x gathered)
+  //   residual          SpMV_l + 8 n          (skipped when pre == 0)
+  //   restriction       SpMV(R_l);  prolongation SpMV(P_l) + 8 n (read-add)
+  //   coarsest          8 n_c^2 + 16 n_c
   double tot = 0;
   for (size_t l = 0; l + 1 < L.size(); ++l) {
     const AmgLevel &v = L[l];
-    double spmv = v.A.bytes_spmv();
-    double sweeps = opts.pre + opts.post;
-    tot += sweeps * (spmv + 24.0 * v.n) + spmv + 8.0 * v.n + v.R.bytes_spmv() + v.P.bytes_spmv() + 16.0 * v.n;
+    double spmv = v.A.bytes_spmv(), n = v.n;
+    double sweeps_spmv = (opts.pre > 0 ? opts.pre - 1 : 0) + opts.post;
+    if (opts.pre > 0) tot += 24.0 * n + spmv + 8.0 * n;
+    tot += sweeps_spmv * (spmv + 16.0 * n) + v.R.bytes_spmv() + v.P.bytes_spmv() + 8.0 * n;
   }
-  tot += 8.0 * (double)cn * cn;
+  tot += 8.0 * (double)cn * cn + 16.0 * cn;
   return tot;
 }
 
@@ -355,8 +362,14 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
   h->post_smoothing = post_smoothing;
   h->coarse_kind = coarse_kind;
   Csr cur = copy_csr(a);
-  std::vector<int64_t> cells(a.nr);
-  for (int i = 0; i < a.nr; ++i) cells[i] = cells_host ? cells_host[i] : i;
+  // per-unknown owning cell, tracked down the levels only when a level relaxes globally
+  bool need_cells = false;
+  for (const LevelSpec &sp : plan) need_cells |= sp.global_relax != 0;
+  std::vector<int64_t> cells;
+  if (need_cells) {
+    cells.resize(a.nr);
+    for (int i = 0; i < a.nr; ++i) cells[i] = cells_host ? cells_host[i] : i;
+  }
   for (const LevelSpec &sp : plan) {
     int n = cur.nr;
     if ((int)sp.fmask.size() != n) throw MgError(MG_ERR_DIM_MISMATCH, "level plan mask length mismatch");
@@ -382,14 +395,13 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
     fsolver_setup(lv.fs, lv.Aff, sp, ao);
     trace("mgr: F-solver setup");
     if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
-    std::vector<int64_t> nxt_cells;
-    {
+    if (need_cells) {
+      std::vector<int64_t> nxt_cells(lv.nc);
       std::vector<int> cl(lv.nc);
       d2h(cl.data(), lv.clist.p, sizeof(int) * lv.nc);
-      nxt_cells.resize(lv.nc);
       for (int c = 0; c < lv.nc; ++c) nxt_cells[c] = cells[cl[c]];
+      cells.swap(nxt_cells);
     }
-    cells.swap(nxt_cells);
     prepare_spmv(cur);
     prepare_spmv(lv.R);
     prepare_spmv(lv.P);

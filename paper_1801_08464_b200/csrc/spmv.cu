@@ -69,6 +69,76 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ row
   }
 }
 
+// ---- SELL-32: one thread per row, loads coalesced across the 32 rows of a slice ----
+template <int UNR, class Epi>
+__global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sptr, const int *__restrict__ rlen,
+                                              const int *__restrict__ ci, const double *__restrict__ v,
+                                              const double *__restrict__ x, Epi epi) {
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nr) return;
+  const int base = __ldg(sptr + (row >> 5)) + (row & 31);
+  const int len = __ldg(rlen + row);
+  double sum = 0.0;
+  int k = 0;
+  for (; k + UNR <= len; k += UNR) {
+    double vv[UNR];
+    int cc[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      vv[u] = __ldcs(v + base + (k + u) * 32);
+      cc[u] = __ldcs(ci + base + (k + u) * 32);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) sum += vv[u] * __ldg(x + cc[u]);
+  }
+  for (; k < len; ++k) sum += __ldcs(v + base + k * 32) * __ldg(x + __ldcs(ci + base + k * 32));
+  epi(row, sum);
+}
+
+// per slice: max row length (warp per slice)
+__global__ void k_sell_len(int nr, int ns, const int *rp, int *rlen, int *slen) {
+  int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (s >= ns) return;
+  int row = s * 32 + lane;
+  int len = row < nr ? rp[row + 1] - rp[row] : 0;
+  if (row < nr) rlen[row] = len;
+  int m = len;
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) slen[s] = m * 32;
+}
+__global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *v, const int *sptr, int *sci,
+                            double *sv) {
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nr) return;
+  int base = sptr[row >> 5] + (row & 31);
+  int s = rp[row], e = rp[row + 1];
+  for (int k = 0; k < e - s; ++k) {
+    sci[base + k * 32] = ci[s + k];
+    sv[base + k * 32] = v[s + k];
+  }
+}
+
+static void build_sell(const Csr &a, SpmvPlan &pl) {
+  int ns = (a.nr + 31) / 32;
+  DBuf<int> slen((size_t)ns + 1);
+  pl.rlen.alloc(a.nr);
+  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p);
+  check_launch("sell_len");
+  DBuf<int64_t> sp64((size_t)ns + 1);
+  int64_t padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
+  if (padded > (int64_t)(1.15 * (double)a.nnz) + 4096 || padded > 2000000000LL) {
+    pl.rlen.release();
+    return;
+  }
+  pl.sptr.alloc((size_t)ns + 1);
+  exclusive_scan_i32_to_i32(slen.p, pl.sptr.p, ns);
+  pl.sci.alloc((size_t)padded);
+  pl.sv.alloc((size_t)padded);
+  k_sell_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, pl.sptr.p, pl.sci.p, pl.sv.p);
+  check_launch("sell_fill");
+  pl.sell = true;
+}
+
 // ---- SpMV plan: rows binned by length class ---------------------------------------
 // class c: len <= 2, 6, 12, 24, 48, 96, >96  ->  (VS, U) below
 __device__ __forceinline__ int len_class(int len) {
@@ -124,6 +194,7 @@ void prepare_spmv(const Csr &a) {
       k_cls_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, cnt.p, pl->rows.p);
       check_launch("cls_fill");
     }
+    if (a.nr >= 32768 && a.nnz >= 4 * (int64_t)a.nr) build_sell(a, *pl);
   }
   a.plan = std::move(pl);
 }
@@ -216,6 +287,14 @@ static void launch_csr(const Csr &a, const double *x, Epi epi) {
   k_csr<VS, U, Epi><<<spmv_grid((int64_t)a.nr * VS), 256, 0, s>>>(a.nr, nullptr, a.rp.p, a.ci.p, a.v.p, x, epi)
   prepare_spmv(a);
   const SpmvPlan &pl = *a.plan;
+  if (pl.sell) {
+    if (avg > 64)
+      k_sell<8, Epi><<<grid_for(a.nr, 128), 128, 0, s>>>(a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
+    else
+      k_sell<4, Epi><<<grid_for(a.nr, 256), 256, 0, s>>>(a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
+    check_launch("sell spmv");
+    return;
+  }
   auto run = [&](int c, int n, const int *rows) {
     if (!n) return;
 #define LAUNCH(VS, U) \
