@@ -191,6 +191,10 @@ typedef struct {
   int64_t vcycle_calls;
   double vcycle_bytes;   /* algorithmic bytes of one coarse V-cycle */
   double spmv_bytes;     /* algorithmic bytes of one BCSR SpMV */
+  /* per-phase device time of the last solve when profiling is on:
+   * 0 BCSR SpMV, 1 coarse AMG cycles, 2 F-relaxation, 3 GMRES orthogonalisation,
+   * 4 MGR level transfers / residuals, 5 prescale, 6 GMRES host sync + Givens, 7 other */
+  double phase_ms[8];
 } mg_timing;
 int mg_get_timing(mg_ctx *ctx, mg_timing *t);
 /* CUDA-event timer on the context stream (bench timed regions) */

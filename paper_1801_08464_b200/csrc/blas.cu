@@ -56,7 +56,20 @@ __global__ void k_scatter_set(double *d, const double *s, const int *idx, int64_
     d[idx[i]] = s[i];
 }
 
+__global__ void k_fc_merge(double *e, const double *ef, const int *fmap, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int f = fmap[i];
+    e[i] = f >= 0 ? ef[f] : 0.0;
+  }
+}
+
 static int ew_grid(int64_t n) { return grid_for(n, 256, g_ctx->num_sms * 8); }
+
+void fc_merge(double *e, const double *ef, const int *fmap, int64_t n) {
+  if (!n) return;
+  k_fc_merge<<<ew_grid(n), 256, 0, stream()>>>(e, ef, fmap, n);
+  check_launch("fc_merge");
+}
 
 void vfill(double *x, double val, int64_t n) {
   if (!n) return;
@@ -164,69 +177,134 @@ double dot(const double *x, const double *y, int64_t n) {
 
 double nrm2(const double *x, int64_t n) { return sqrt(dot(x, x, n)); }
 
-// partial projections of w onto V_0..V_{K-1} (K <= 32 per pass)
-template <int KM>
-__global__ void __launch_bounds__(RB) k_mdot(const double *__restrict__ V, int64_t ldv, int K,
-                                            const double *__restrict__ w, int64_t n,
-                                            double *partial) {
-  double acc[KM];
-#pragma unroll
-  for (int k = 0; k < KM; ++k) acc[k] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-    double wi = w[i];
-#pragma unroll
-    for (int k = 0; k < KM; ++k)
-      if (k < K) acc[k] += V[k * ldv + i] * wi;
-  }
-  block_reduce_store<KM>(acc, K, partial);
-}
+// Projections onto V_0..V_{K-1} (K <= 32) with a shared-memory tile of V:
+// each thread stages V[k][i] for its element i (coalesced across the block),
+// optionally folding it into w_i -= sum_k c_k V_k[i] on the way; then warp q
+// forms the dot products of vectors q, q+8, q+16, q+24 with the tile of w.
+// Registers stay low (the previous register-resident version sat at 202
+// registers / 12% occupancy); V and w are read once.
+static const int OT = 256;  // elements per tile == threads per block
 
-// w -= sum c_k V_k ; then partial V^T w
-template <int KM>
-__global__ void __launch_bounds__(RB) k_update_mdot(const double *__restrict__ V, int64_t ldv, int K,
-                                                   const double *__restrict__ c, double *w,
-                                                   int64_t n, double *partial) {
-  __shared__ double cc[KM];
-  double acc[KM];
-  if (threadIdx.x < KM) cc[threadIdx.x] = (int)threadIdx.x < K ? c[threadIdx.x] : 0.0;
+template <bool UPDATE>
+__global__ void __launch_bounds__(OT) k_ortho(const double *__restrict__ V, int64_t ldv, int K,
+                                             const double *__restrict__ c, double *w, int64_t n,
+                                             double *partial) {
+  extern __shared__ __align__(16) double osm[];
+  double *vt = osm;              // [32][OT]
+  double *wt = osm + 32 * OT;    // [OT]
+  __shared__ double cc[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (UPDATE && tid < 32) cc[tid] = tid < K ? c[tid] : 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   __syncthreads();
+  for (int64_t t0 = (int64_t)blockIdx.x * OT; t0 < n; t0 += (int64_t)gridDim.x * OT) {
+    int64_t i = t0 + tid;
+    bool ok = i < n;
+    double s = 0.0;
+    // 8 independent loads in flight before their shared-memory stores
+    for (int k0 = 0; k0 < K; k0 += 8) {
+      double vk[8];
 #pragma unroll
-  for (int k = 0; k < KM; ++k) acc[k] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-    double vk[KM];
-    double t = 0.0;
+      for (int u = 0; u < 8; ++u) vk[u] = (ok && k0 + u < K) ? __ldcs(V + (k0 + u) * ldv + i) : 0.0;
 #pragma unroll
-    for (int k = 0; k < KM; ++k) {
-      vk[k] = k < K ? V[k * ldv + i] : 0.0;
-      t += cc[k] * vk[k];
+      for (int u = 0; u < 8; ++u) {
+        if (k0 + u < K) {
+          vt[(k0 + u) * OT + tid] = vk[u];
+          if (UPDATE) s += cc[k0 + u] * vk[u];
+        }
+      }
     }
-    double wi = w[i] - t;
-    w[i] = wi;
+    double wi = ok ? w[i] : 0.0;
+    if (UPDATE) {
+      wi -= s;
+      if (ok) w[i] = wi;
+    }
+    wt[tid] = wi;
+    __syncthreads();
 #pragma unroll
-    for (int k = 0; k < KM; ++k) acc[k] += vk[k] * wi;
+    for (int q = 0; q < 4; ++q) {
+      int k = wid + 8 * q;
+      if (k < K)
+        for (int e = lane; e < OT; e += 32) acc[q] += vt[k * OT + e] * wt[e];
+    }
+    __syncthreads();
   }
-  block_reduce_store<KM>(acc, K, partial);
+  // every vector k is owned by one warp: reduce over lanes, write the block partial
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double a = acc[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
+    int k = wid + 8 * q;
+    if (lane == 0 && k < K) partial[(int64_t)blockIdx.x * K + k] = a;
+  }
 }
 
-// w -= sum c_k V_k ; partial ||w||^2
-template <int KM>
+// w -= sum c_k V_k ; partial ||w||^2  (c staged in shared memory, low registers)
 __global__ void __launch_bounds__(RB) k_update_norm(const double *__restrict__ V, int64_t ldv, int K,
-                                                   const double *__restrict__ c, double *w,
-                                                   int64_t n, double *partial) {
-  double cc[KM];
-#pragma unroll
-  for (int k = 0; k < KM; ++k) cc[k] = k < K ? c[k] : 0.0;
+                                                   const double *__restrict__ c, double *w, int64_t n,
+                                                   double *partial) {
+  __shared__ double cc[32];
+  if (threadIdx.x < 32) cc[threadIdx.x] = (int)threadIdx.x < K ? c[threadIdx.x] : 0.0;
+  __syncthreads();
   double acc[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-    double t = 0.0;
+  // two consecutive elements per thread (16-byte loads) when ldv and n are even
+  if ((ldv & 1) == 0) {
+    const int64_t n2 = n >> 1;
+    const double2 *V2 = reinterpret_cast<const double2 *>(V);
+    double2 *w2 = reinterpret_cast<double2 *>(w);
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n2; i += (int64_t)gridDim.x * RB) {
+      double tx = 0.0, ty = 0.0;
+      for (int k0 = 0; k0 < K; k0 += 8) {
+        double2 vk[8];
 #pragma unroll
-    for (int k = 0; k < KM; ++k)
-      if (k < K) t += cc[k] * V[k * ldv + i];
-    double wi = w[i] - t;
-    w[i] = wi;
-    acc[0] += wi * wi;
+        for (int u = 0; u < 8; ++u)
+          vk[u] = k0 + u < K ? __ldcs(V2 + (k0 + u) * (ldv >> 1) + i) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          tx += cc[k0 + u < 32 ? k0 + u : 31] * vk[u].x;
+          ty += cc[k0 + u < 32 ? k0 + u : 31] * vk[u].y;
+        }
+      }
+      double2 wv = w2[i];
+      wv.x -= tx;
+      wv.y -= ty;
+      w2[i] = wv;
+      acc[0] += wv.x * wv.x + wv.y * wv.y;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      int64_t i = n - 1;
+      double t = 0.0;
+      for (int k = 0; k < K; ++k) t += cc[k] * V[k * ldv + i];
+      double wi = w[i] - t;
+      w[i] = wi;
+      acc[0] += wi * wi;
+    }
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+      double t = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < K; ++k) t += cc[k] * V[k * ldv + i];
+      double wi = w[i] - t;
+      w[i] = wi;
+      acc[0] += wi * wi;
+    }
   }
   block_reduce_store<1>(acc, 1, partial);
+}
+
+static int ortho_blocks(int64_t n) {
+  int64_t b = (n + OT - 1) / OT;
+  int cap = g_ctx->num_sms * 3;
+  return (int)(b > cap ? cap : (b < 1 ? 1 : b));
+}
+static size_t ortho_smem() { return sizeof(double) * (32 * OT + OT); }
+static void ortho_attr() {
+  static bool done = false;
+  if (done) return;
+  MG_CUDA(cudaFuncSetAttribute(k_ortho<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ortho_smem()));
+  MG_CUDA(cudaFuncSetAttribute(k_ortho<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ortho_smem()));
+  done = true;
 }
 
 // u = sum y_k V_k (or u += when accumulate)
@@ -250,13 +328,13 @@ __global__ void __launch_bounds__(RB) k_combine(const double *__restrict__ V, in
   do { if ((K) <= 16) { CALL16; } else { CALL32; } } while (0)
 
 void mdot(const double *V, int64_t ldv, int K, const double *w, int64_t n, double *out_dev) {
-  int nb = red_blocks(n);
+  ortho_attr();
+  int nb = ortho_blocks(n);
   for (int k0 = 0; k0 < K; k0 += 32) {
     int kk = K - k0 < 32 ? K - k0 : 32;
     double *part = red_scratch((size_t)nb * 32);
     const double *Vk = V + (int64_t)k0 * ldv;
-    KSEL(kk, (k_mdot<16><<<nb, RB, 0, stream()>>>(Vk, ldv, kk, w, n, part)),
-         (k_mdot<32><<<nb, RB, 0, stream()>>>(Vk, ldv, kk, w, n, part)));
+    k_ortho<false><<<nb, OT, ortho_smem(), stream()>>>(Vk, ldv, kk, nullptr, const_cast<double *>(w), n, part);
     check_launch("mdot");
     reduce_finish(part, nb, kk, out_dev + k0);
   }
@@ -264,11 +342,11 @@ void mdot(const double *V, int64_t ldv, int K, const double *w, int64_t n, doubl
 
 void update_mdot(const double *V, int64_t ldv, int K, const double *c_dev, double *w, int64_t n,
                  double *out_dev) {
-  int nb = red_blocks(n);
   if (K <= 32) {
+    ortho_attr();
+    int nb = ortho_blocks(n);
     double *part = red_scratch((size_t)nb * 32);
-    KSEL(K, (k_update_mdot<16><<<nb, RB, 0, stream()>>>(V, ldv, K, c_dev, w, n, part)),
-         (k_update_mdot<32><<<nb, RB, 0, stream()>>>(V, ldv, K, c_dev, w, n, part)));
+    k_ortho<true><<<nb, OT, ortho_smem(), stream()>>>(V, ldv, K, c_dev, w, n, part);
     check_launch("update_mdot");
     reduce_finish(part, nb, K, out_dev);
     return;
@@ -285,8 +363,7 @@ void update_norm2(const double *V, int64_t ldv, int K, const double *c_dev, doub
   int nb = red_blocks(n);
   double *part = red_scratch((size_t)nb + 8);
   if (K <= 32) {
-    KSEL(K, (k_update_norm<16><<<nb, RB, 0, stream()>>>(V, ldv, K, c_dev, w, n, part)),
-         (k_update_norm<32><<<nb, RB, 0, stream()>>>(V, ldv, K, c_dev, w, n, part)));
+    k_update_norm<<<nb, RB, 0, stream()>>>(V, ldv, K, c_dev, w, n, part);
     check_launch("update_norm");
     reduce_finish(part, nb, 1, out_dev);
     return;

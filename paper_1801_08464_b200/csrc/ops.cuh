@@ -27,6 +27,8 @@ void vsub(double *r, const double *b, const double *ax, int64_t n);         // r
 void gather(double *dst, const double *src, const int *idx, int64_t n);     // dst[i] = src[idx[i]]
 void scatter_add(double *dst, const double *src, const int *idx, int64_t n);// dst[idx[i]] += src[i]
 void scatter_set(double *dst, const double *src, const int *idx, int64_t n);// dst[idx[i]] = src[i]
+// e[i] = fmap[i] >= 0 ? ef[fmap[i]] : 0   (F values into a zeroed full vector, one pass)
+void fc_merge(double *e, const double *ef, const int *fmap, int64_t n);
 // deterministic reductions; result left in device memory `out` (and returned when host=true)
 double dot(const double *x, const double *y, int64_t n);
 double nrm2(const double *x, int64_t n);

@@ -15,7 +15,6 @@ namespace mg {
 static const int DENSE_LIMIT = 8192;
 
 // ---- profiling of hot kernels ---------------------------------------------------
-static thread_local std::vector<ProfScope *> *g_open = nullptr;
 struct ProfRec { int kind; cudaEvent_t a, b; };
 static thread_local std::vector<ProfRec> g_prof;
 
@@ -35,6 +34,7 @@ void prof_reset() {
   g_prof.clear();
   g_ctx->timing.spmv_ms = g_ctx->timing.vcycle_ms = 0;
   g_ctx->timing.spmv_calls = g_ctx->timing.vcycle_calls = 0;
+  for (double &p : g_ctx->timing.phase_ms) p = 0.0;
 }
 void prof_collect() {
   if (g_prof.empty()) return;
@@ -42,8 +42,9 @@ void prof_collect() {
   for (auto &r : g_prof) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
+    if (r.kind >= 0 && r.kind < 8) g_ctx->timing.phase_ms[r.kind] += ms;
     if (r.kind == 0) { g_ctx->timing.spmv_ms += ms; g_ctx->timing.spmv_calls++; }
-    else { g_ctx->timing.vcycle_ms += ms; g_ctx->timing.vcycle_calls++; }
+    else if (r.kind == 1) { g_ctx->timing.vcycle_ms += ms; g_ctx->timing.vcycle_calls++; }
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
@@ -381,7 +382,8 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
     lv.rp = sp.rp;
     DBuf<uint8_t> mask(n);
     h2d(mask.p, sp.fmask.data(), n);
-    DBuf<int> fmap, cmap;
+    DBuf<int> cmap;
+    DBuf<int> &fmap = lv.fmap;
     fc_split(mask.p, n, lv.flist, lv.clist, fmap, cmap, lv.nf, lv.nc);
     trace("mgr: fc_split");
     build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
@@ -452,21 +454,28 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
     return lv.res.p;
   };
   auto f_relax = [&]() {
-    const double *rr = resid();
-    gather(lv.rF.p, rr, lv.flist.p, lv.nf);
-    fsolve(lv.fs, lv.Aff, lv.rF.p, lv.eF.p);
-    if (zero) {
-      vfill(e, 0.0, lv.n);
-      scatter_set(e, lv.eF.p, lv.flist.p, lv.nf);
-    } else {
-      scatter_add(e, lv.eF.p, lv.flist.p, lv.nf);
+    {
+      ProfScope ps(4);
+      const double *rr = resid();
+      gather(lv.rF.p, rr, lv.flist.p, lv.nf);
     }
+    {
+      ProfScope ps(2);
+      fsolve(lv.fs, lv.Aff, lv.rF.p, lv.eF.p);
+    }
+    ProfScope ps(4);
+    if (zero) fc_merge(e, lv.eF.p, lv.fmap.p, lv.n);  // e = [e_F; 0] in one pass
+    else scatter_add(e, lv.eF.p, lv.flist.p, lv.nf);
     zero = false;
   };
   auto coarse_correct = [&]() {
-    const double *rr = resid();
-    spmv(lv.R, rr, lv.rc.p);
+    {
+      ProfScope ps(4);
+      const double *rr = resid();
+      spmv(lv.R, rr, lv.rc.p);
+    }
     apply_level(h, k + 1, lv.rc.p, lv.ec.p);
+    ProfScope ps(4);
     if (zero) spmv(lv.P, lv.ec.p, e);
     else spmv_add(lv.P, lv.ec.p, e);
     zero = false;
@@ -483,6 +492,7 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
 void mgr_apply(Mgr &h, const double *r, double *e) {
   const double *rr = r;
   if (h.has_prescale) {
+    ProfScope ps(5);
     block_apply(h.prescale, r, h.pre_buf.p);
     rr = h.pre_buf.p;
   }
@@ -516,7 +526,9 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
     return use_anorm && res <= o.rel_tol * (a_norm * xn + b_norm);
   };
   int mmax = std::min(o.restart, o.max_iter);
-  DBuf<double> V((size_t)(mmax + 1) * n), w(n), z(n), r(n), xt(n), u(n), t(n), proj((size_t)2 * (mmax + 1) + 8);
+  // basis row stride padded off a power of two (K streams 32 MB apart otherwise collide)
+  const int64_t ldv = ((n + 1) & ~(int64_t)1) + 1024;
+  DBuf<double> V((size_t)(mmax + 1) * ldv), w(n), z(n), r(n), xt(n), u(n), t(n), proj((size_t)2 * (mmax + 1) + 8);
   double *c_dev = proj.p, *c2_dev = proj.p + (mmax + 1), *nrm_dev = proj.p + 2 * (mmax + 1);
   std::vector<double> hbuf(2 * (mmax + 1) + 1);
   vfill(x, 0.0, n);
@@ -563,7 +575,7 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
       }
       if (k) {
         h2d(c_dev, y.data(), sizeof(double) * k);
-        combine(V.p, n, k, c_dev, u.p, n);
+        combine(V.p, ldv, k, c_dev, u.p, n);
       } else {
         vfill(u.p, 0.0, n);
       }
@@ -575,18 +587,24 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
     bool early = false;
     double early_res = 0.0;
     for (int j = 0; j < mm; ++j) {
-      double *vj = V.p + (int64_t)j * n;
+      double *vj = V.p + (int64_t)j * ldv;
       const double *mz = precond(vj, z.p);
       op_apply(a, mz, w.p);
       int K = j + 1;
-      mdot(V.p, n, K, w.p, n, c_dev);
-      if (o.reorth) {
-        update_mdot(V.p, n, K, c_dev, w.p, n, c2_dev);
-        update_norm2(V.p, n, K, c2_dev, w.p, n, nrm_dev);
-      } else {
-        update_norm2(V.p, n, K, c_dev, w.p, n, nrm_dev);
+      {
+        ProfScope ps(3);
+        mdot(V.p, ldv, K, w.p, n, c_dev);
+        if (o.reorth) {
+          update_mdot(V.p, ldv, K, c_dev, w.p, n, c2_dev);
+          update_norm2(V.p, ldv, K, c2_dev, w.p, n, nrm_dev);
+        } else {
+          update_norm2(V.p, ldv, K, c_dev, w.p, n, nrm_dev);
+        }
       }
-      d2h(hbuf.data(), proj.p, sizeof(double) * (2 * (mmax + 1) + 1));
+      {
+        ProfScope ps(6);
+        d2h(hbuf.data(), proj.p, sizeof(double) * (2 * (mmax + 1) + 1));
+      }
       for (int i = 0; i < K; ++i) h_at(i, j) = o.reorth ? hbuf[i] + hbuf[(mmax + 1) + i] : hbuf[i];
       double hn = std::sqrt(hbuf[2 * (mmax + 1)]);
       h_at(j + 1, j) = hn;
@@ -621,7 +639,7 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
           break;
         }
       }
-      vdiv_scalar(V.p + (int64_t)(j + 1) * n, w.p, hn, n);
+      vdiv_scalar(V.p + (int64_t)(j + 1) * ldv, w.p, hn, n);
     }
     if (early) {
       vcopy(x, xt.p, n);

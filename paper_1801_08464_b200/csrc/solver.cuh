@@ -62,7 +62,7 @@ struct BlockDiag {             // per-cell block-diagonal relaxation (mgr.py:212
 struct MgrLevel {
   Csr A, R, P, Aff;
   int n = 0, nf = 0, nc = 0, rp = 0;
-  DBuf<int> flist, clist;
+  DBuf<int> flist, clist, fmap;
   FSolver fs;
   std::unique_ptr<BlockDiag> bd;
   DBuf<double> res, rF, eF, rc, ec;

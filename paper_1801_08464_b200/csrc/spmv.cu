@@ -126,7 +126,13 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   check_launch("sell_len");
   DBuf<int64_t> sp64((size_t)ns + 1);
   int64_t padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
-  if (padded > (int64_t)(1.15 * (double)a.nnz) + 4096 || padded > 2000000000LL) {
+  // padded slots beyond a row's length are never loaded (predicated by rlen), so
+  // padding costs footprint and idle lanes, not bandwidth: accept up to 2x for
+  // short rows (where CSR lane groups are inefficient), 1.15x otherwise
+  // (measured: irregular long-row coarse levels lose with SELL)
+  double avg = (double)a.nnz / (a.nr ? a.nr : 1);
+  double cap = avg <= 16.0 ? 2.0 : 1.15;
+  if (padded > (int64_t)(cap * (double)a.nnz) + 4096 || padded > 2000000000LL) {
     pl.rlen.release();
     return;
   }
