@@ -394,6 +394,7 @@ int mg_mgr_set_prescale(mg_ctx *ctx, mg_mgr *h, const mg_mat *dinv) {
     if (vec_len(dinv->m) != h->h->n0) throw MgError(MG_ERR_DIM_MISMATCH, "prescale dimension mismatch");
     h->h->prescale = copy_csr(dinv->m);
     h->h->has_prescale = true;
+    h->h->drop_graph();
     h->h->pre_buf.alloc((size_t)h->h->n0);
   });
 }

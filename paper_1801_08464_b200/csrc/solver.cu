@@ -489,7 +489,7 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
   }
 }
 
-void mgr_apply(Mgr &h, const double *r, double *e) {
+static void mgr_apply_direct(Mgr &h, const double *r, double *e) {
   const double *rr = r;
   if (h.has_prescale) {
     ProfScope ps(5);
@@ -497,6 +497,76 @@ void mgr_apply(Mgr &h, const double *r, double *e) {
     rr = h.pre_buf.p;
   }
   apply_level(h, 0, rr, e);
+}
+
+void Mgr::drop_graph() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  gexec = nullptr;
+}
+Mgr::~Mgr() { drop_graph(); }
+
+static bool graphs_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_GRAPHS");
+    on = !(e && *e == '0');
+  }
+  return on != 0;
+}
+
+// Capture one apply (gin -> gout) as a CUDA graph: the ~100 dependent kernel
+// launches of an MGR + 2 AMG cycles replay with minimal inter-kernel gaps.
+static bool capture_apply(Mgr &h) {
+  if (!h.gin.p) {
+    h.gin.alloc((size_t)h.n0);
+    h.gout.alloc((size_t)h.n0);
+  }
+  cudaGraph_t graph = nullptr;
+  int64_t l0 = g_ctx->launches;
+  if (cudaStreamBeginCapture(stream(), cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  bool ok = true;
+  try {
+    mgr_apply_direct(h, h.gin.p, h.gout.p);
+  } catch (...) {
+    ok = false;
+  }
+  cudaError_t e = cudaStreamEndCapture(stream(), &graph);
+  if (!ok || e != cudaSuccess || !graph) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    g_ctx->launches = l0;
+    return false;
+  }
+  e = cudaGraphInstantiate(&h.gexec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    h.gexec = nullptr;
+    g_ctx->launches = l0;
+    return false;
+  }
+  h.graph_kernels = g_ctx->launches - l0;
+  g_ctx->launches = l0;
+  return true;
+}
+
+void mgr_apply(Mgr &h, const double *r, double *e) {
+  if (g_ctx->profiling || !graphs_enabled() || h.graph_failed) {
+    mgr_apply_direct(h, r, e);
+    return;
+  }
+  if (!h.gexec && !capture_apply(h)) {
+    h.graph_failed = true;
+    mgr_apply_direct(h, r, e);
+    return;
+  }
+  if (r != h.gin.p) vcopy(h.gin.p, r, h.n0);
+  MG_CUDA(cudaGraphLaunch(h.gexec, stream()));
+  g_ctx->launches += h.graph_kernels;
+  if (e != h.gout.p) vcopy(e, h.gout.p, h.n0);
 }
 
 // ================================ GMRES ============================================

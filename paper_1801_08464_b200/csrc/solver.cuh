@@ -80,6 +80,13 @@ struct Mgr {
   Csr prescale;                // optional per-cell D^-1 (block diagonal)
   bool has_prescale = false;
   DBuf<double> pre_buf;
+  // CUDA graph of one apply (fixed in/out buffers), captured on first use
+  cudaGraphExec_t gexec = nullptr;
+  DBuf<double> gin, gout;
+  int64_t graph_kernels = 0;
+  bool graph_failed = false;
+  ~Mgr();
+  void drop_graph();
 };
 
 std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan, const AmgOpts &ao,
