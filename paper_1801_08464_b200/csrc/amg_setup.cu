@@ -380,23 +380,72 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
     double aii = bal ? __dadd_rn(0.0, v[__shfl_sync(0xffffffffu, found, __ffs(bal) - 1)]) : 0.0;
     dt = __dadd_rn(aii, lump);
   }
-  // distribution through strong F neighbours k, in row-i order
-  for (int q = b; q < e; ++q) {
-    int k = ci[q];
-    if (k == i || !s[q] || state[k] != FPT) continue;
-    double aik = v[q];
-    int kb = rp[k], ke = rp[k + 1];
-    // a_kk (single stored diagonal, 0 when absent)
-    int found = -1;
-    for (int q2 = kb + lane; q2 < ke; q2 += 32)
-      if (ci[q2] == k) found = q2;
-    unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
-    double akk = bal ? __dadd_rn(0.0, v[__shfl_sync(0xffffffffu, found, __ffs(bal) - 1)]) : 0.0;
+  // distribution through strong F neighbours k, in row-i order.  The strong-F
+  // entries of a 32-entry chunk of row i are found with one ballot (their row
+  // ranges prefetched by their own lanes); a row k of <= 64 entries is held in
+  // registers (two entries per lane) for a_kk, beta_k, the numerators and the
+  // a_ki term, so each k costs a single round trip to memory.
+  for (int q0 = b; q0 < e; q0 += 32) {
+    int qq = q0 + lane;
+    int kk = -1, kb_l = 0, ke_l = 0;
+    double aik_l = 0.0;
+    if (qq < e) {
+      int j = ci[qq];
+      if (j != i && s[qq] && state[j] == FPT) {
+        kk = j;
+        aik_l = v[qq];
+        kb_l = rp[j];
+        ke_l = rp[j + 1];
+      }
+    }
+    unsigned kmask = __ballot_sync(0xffffffffu, kk >= 0);
+    while (kmask) {
+      int src = __ffs(kmask) - 1;
+      kmask &= kmask - 1;
+      int k = __shfl_sync(0xffffffffu, kk, src);
+      double aik = __shfl_sync(0xffffffffu, aik_l, src);
+      int kb = __shfl_sync(0xffffffffu, kb_l, src), ke = __shfl_sync(0xffffffffu, ke_l, src);
+      int len = ke - kb;
+      if (len <= 64) {
+        int l0 = -1, l1 = -1;
+        double v0 = 0.0, v1 = 0.0;
+        if (lane < len) { l0 = ci[kb + lane]; v0 = v[kb + lane]; }
+        if (lane + 32 < len) { l1 = ci[kb + 32 + lane]; v1 = v[kb + 32 + lane]; }
+        unsigned db = __ballot_sync(0xffffffffu, l0 == k || l1 == k);
+        double dv = l0 == k ? v0 : v1;
+        double akk = db ? __dadd_rn(0.0, __shfl_sync(0xffffffffu, dv, __ffs(db) - 1)) : 0.0;
+        bool o0 = l0 >= 0 && l0 != k && opposite(v0, akk);
+        bool o1 = l1 >= 0 && l1 != k && opposite(v1, akk);
+        int s0 = o0 && l0 != i ? hash_find_opt(t.keys, mask, l0) : -1;
+        int s1 = o1 && l1 != i ? hash_find_opt(t.keys, mask, l1) : -1;
+        double beta = __dadd_rn(0.0, warp_tree(o0 && (l0 == i || s0 >= 0) ? v0 : 0.0));
+        if (len > 32) beta = __dadd_rn(beta, warp_tree(o1 && (l1 == i || s1 >= 0) ? v1 : 0.0));
+        if (beta == 0.0) {
+          dt = __dadd_rn(dt, aik);
+          continue;
+        }
+        double f = __ddiv_rn(aik, beta);
+        if (s0 >= 0) { int p = t.pos[s0]; num[p] = __dadd_rn(num[p], __dmul_rn(f, v0)); }
+        if (s1 >= 0) { int p = t.pos[s1]; num[p] = __dadd_rn(num[p], __dmul_rn(f, v1)); }
+        unsigned bi = __ballot_sync(0xffffffffu, (o0 && l0 == i) || (o1 && l1 == i));
+        if (bi) {
+          double iv = (o0 && l0 == i) ? v0 : v1;
+          dt = __dadd_rn(dt, __dmul_rn(f, __shfl_sync(0xffffffffu, iv, __ffs(bi) - 1)));
+        }
+        __syncwarp();
+        continue;
+      }
+      // long rows: chunked reloads
+      int found = -1;
+      for (int q2 = kb + lane; q2 < ke; q2 += 32)
+        if (ci[q2] == k) found = q2;
+      unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
+      double akk = bal ? __dadd_rn(0.0, v[__shfl_sync(0xffffffffu, found, __ffs(bal) - 1)]) : 0.0;
     // beta = TREE over row k of abar_kl for l in Chat u {i}
     double beta = 0.0;
     int at_i = -1;
-    for (int q0 = kb; q0 < ke; q0 += 32) {
-      int q2 = q0 + lane;
+    for (int c0 = kb; c0 < ke; c0 += 32) {
+      int q2 = c0 + lane;
       double term = 0.0;
       if (q2 < ke) {
         int l = ci[q2];
@@ -424,6 +473,7 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
     unsigned bi = __ballot_sync(0xffffffffu, at_i >= 0);
     if (bi) dt = __dadd_rn(dt, __dmul_rn(f, v[__shfl_sync(0xffffffffu, at_i, __ffs(bi) - 1)]));
     __syncwarp();
+    }
   }
   if (dt == 0.0) {
     if (lane == 0) atomicMin(A.bad, i);
