@@ -13,7 +13,7 @@ namespace mg {
 static const int RB = 256;           // threads per reduction block
 static int red_blocks(int64_t n) {
   int64_t b = (n + RB * 4 - 1) / (RB * 4);
-  int cap = g_ctx->num_sms * 4;
+  int cap = g_ctx->num_sms * 8;
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   return (int)b;
@@ -240,6 +240,61 @@ __global__ void __launch_bounds__(OT) k_ortho(const double *__restrict__ V, int6
   }
 }
 
+// c_k = V_k . w for k < K <= 32: warp q of the block owns vectors q, q+8,
+// q+16, q+24 over the block's chunk of CH elements; w is re-read from L1 by
+// the 8 warps, V streams once; 4 accumulators per thread, full occupancy.
+static const int MCH = 2048;
+__global__ void __launch_bounds__(256) k_mdot2(const double *__restrict__ V, int64_t ldv, int K,
+                                              const double *__restrict__ w, int64_t n, double *partial) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t c0 = (int64_t)blockIdx.x * MCH; c0 < n; c0 += (int64_t)gridDim.x * MCH) {
+    int64_t cend = c0 + MCH < n ? c0 + MCH : n;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int k = wid + 8 * q;
+      if (k >= K) break;
+      const double *vk = V + k * ldv;
+      double a = 0.0;
+      int64_t i = c0 + lane;
+      for (; i + 96 < cend; i += 128) {
+        double v0 = __ldcs(vk + i), v1 = __ldcs(vk + i + 32), v2 = __ldcs(vk + i + 64), v3 = __ldcs(vk + i + 96);
+        double w0 = __ldg(w + i), w1 = __ldg(w + i + 32), w2 = __ldg(w + i + 64), w3 = __ldg(w + i + 96);
+        a += v0 * w0 + v1 * w1 + v2 * w2 + v3 * w3;
+      }
+      for (; i < cend; i += 32) a += __ldcs(vk + i) * __ldg(w + i);
+      acc[q] += a;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double a = acc[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
+    int k = wid + 8 * q;
+    if (lane == 0 && k < K) partial[(int64_t)blockIdx.x * K + k] = a;
+  }
+}
+
+// w -= sum_k c_k V_k (streaming, two elements per thread)
+__global__ void __launch_bounds__(RB) k_update(const double *__restrict__ V, int64_t ldv, int K,
+                                              const double *__restrict__ c, double *w, int64_t n) {
+  __shared__ double cc[32];
+  if (threadIdx.x < 32) cc[threadIdx.x] = (int)threadIdx.x < K ? c[threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+    double t = 0.0;
+    for (int k0 = 0; k0 < K; k0 += 8) {
+      double vk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) vk[u] = k0 + u < K ? __ldcs(V + (k0 + u) * ldv + i) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t += cc[(k0 + u) & 31] * vk[u];
+    }
+    w[i] = w[i] - t;
+  }
+}
+
 // w -= sum c_k V_k ; partial ||w||^2  (c staged in shared memory, low registers)
 __global__ void __launch_bounds__(RB) k_update_norm(const double *__restrict__ V, int64_t ldv, int K,
                                                    const double *__restrict__ c, double *w, int64_t n,
@@ -328,13 +383,13 @@ __global__ void __launch_bounds__(RB) k_combine(const double *__restrict__ V, in
   do { if ((K) <= 16) { CALL16; } else { CALL32; } } while (0)
 
 void mdot(const double *V, int64_t ldv, int K, const double *w, int64_t n, double *out_dev) {
-  ortho_attr();
-  int nb = ortho_blocks(n);
+  int64_t want = (n + MCH - 1) / MCH;
+  int nb = (int)(want < g_ctx->num_sms * 8 ? (want < 1 ? 1 : want) : g_ctx->num_sms * 8);
   for (int k0 = 0; k0 < K; k0 += 32) {
     int kk = K - k0 < 32 ? K - k0 : 32;
     double *part = red_scratch((size_t)nb * 32);
     const double *Vk = V + (int64_t)k0 * ldv;
-    k_ortho<false><<<nb, OT, ortho_smem(), stream()>>>(Vk, ldv, kk, nullptr, const_cast<double *>(w), n, part);
+    k_mdot2<<<nb, 256, 0, stream()>>>(Vk, ldv, kk, w, n, part);
     check_launch("mdot");
     reduce_finish(part, nb, kk, out_dev + k0);
   }
@@ -343,12 +398,10 @@ void mdot(const double *V, int64_t ldv, int K, const double *w, int64_t n, doubl
 void update_mdot(const double *V, int64_t ldv, int K, const double *c_dev, double *w, int64_t n,
                  double *out_dev) {
   if (K <= 32) {
-    ortho_attr();
-    int nb = ortho_blocks(n);
-    double *part = red_scratch((size_t)nb * 32);
-    k_ortho<true><<<nb, OT, ortho_smem(), stream()>>>(V, ldv, K, c_dev, w, n, part);
-    check_launch("update_mdot");
-    reduce_finish(part, nb, K, out_dev);
+    // w -= cV (one streaming pass), then the projections of the updated w
+    k_update<<<grid_for(n, RB, g_ctx->num_sms * 8), RB, 0, stream()>>>(V, ldv, K, c_dev, w, n);
+    check_launch("update");
+    mdot(V, ldv, K, w, n, out_dev);
     return;
   }
   // long restarts: unfused (w -= cV chunk by chunk, then projections)
