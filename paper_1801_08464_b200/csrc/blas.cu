@@ -2,10 +2,12 @@
 // (krylov.py:101-109: c = V w; w -= c V; c' = V w; w -= c' V; h = ||w||).
 //
 // Reductions are two-stage with a fixed block count and fixed order, so every
-// result is bitwise reproducible run to run.  The projection of step j reads
-// the j+1 basis vectors once per pass: update_mdot fuses "w -= cV" with the
-// re-orthogonalisation dot products and update_norm2 fuses the second
-// subtraction with ||w||^2 (3 basis passes per Arnoldi step instead of 5).
+// result is bitwise reproducible run to run.  An Arnoldi step makes four
+// streaming passes over its j+1 basis vectors: mdot (c = V w), update
+// (w -= c V), mdot (c' = V w), update_norm2 (w -= c' V fused with ||w||^2).
+// The register-light mdot (4 accumulators, w shared through L1) measured
+// faster than a 3-pass variant that kept all j+1 vectors in registers or
+// shared memory (202 registers / 12% occupancy, resp. 37% occupancy).
 #include "ops.cuh"
 
 namespace mg {
@@ -177,69 +179,6 @@ double dot(const double *x, const double *y, int64_t n) {
 
 double nrm2(const double *x, int64_t n) { return sqrt(dot(x, x, n)); }
 
-// Projections onto V_0..V_{K-1} (K <= 32) with a shared-memory tile of V:
-// each thread stages V[k][i] for its element i (coalesced across the block),
-// optionally folding it into w_i -= sum_k c_k V_k[i] on the way; then warp q
-// forms the dot products of vectors q, q+8, q+16, q+24 with the tile of w.
-// Registers stay low (the previous register-resident version sat at 202
-// registers / 12% occupancy); V and w are read once.
-static const int OT = 256;  // elements per tile == threads per block
-
-template <bool UPDATE>
-__global__ void __launch_bounds__(OT) k_ortho(const double *__restrict__ V, int64_t ldv, int K,
-                                             const double *__restrict__ c, double *w, int64_t n,
-                                             double *partial) {
-  extern __shared__ __align__(16) double osm[];
-  double *vt = osm;              // [32][OT]
-  double *wt = osm + 32 * OT;    // [OT]
-  __shared__ double cc[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (UPDATE && tid < 32) cc[tid] = tid < K ? c[tid] : 0.0;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  __syncthreads();
-  for (int64_t t0 = (int64_t)blockIdx.x * OT; t0 < n; t0 += (int64_t)gridDim.x * OT) {
-    int64_t i = t0 + tid;
-    bool ok = i < n;
-    double s = 0.0;
-    // 8 independent loads in flight before their shared-memory stores
-    for (int k0 = 0; k0 < K; k0 += 8) {
-      double vk[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) vk[u] = (ok && k0 + u < K) ? __ldcs(V + (k0 + u) * ldv + i) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (k0 + u < K) {
-          vt[(k0 + u) * OT + tid] = vk[u];
-          if (UPDATE) s += cc[k0 + u] * vk[u];
-        }
-      }
-    }
-    double wi = ok ? w[i] : 0.0;
-    if (UPDATE) {
-      wi -= s;
-      if (ok) w[i] = wi;
-    }
-    wt[tid] = wi;
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int k = wid + 8 * q;
-      if (k < K)
-        for (int e = lane; e < OT; e += 32) acc[q] += vt[k * OT + e] * wt[e];
-    }
-    __syncthreads();
-  }
-  // every vector k is owned by one warp: reduce over lanes, write the block partial
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    double a = acc[q];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) a += __shfl_down_sync(0xffffffffu, a, off);
-    int k = wid + 8 * q;
-    if (lane == 0 && k < K) partial[(int64_t)blockIdx.x * K + k] = a;
-  }
-}
-
 // c_k = V_k . w for k < K <= 32: warp q of the block owns vectors q, q+8,
 // q+16, q+24 over the block's chunk of CH elements; w is re-read from L1 by
 // the 8 warps, V streams once; 4 accumulators per thread, full occupancy.
@@ -346,20 +285,6 @@ __global__ void __launch_bounds__(RB) k_update_norm(const double *__restrict__ V
     }
   }
   block_reduce_store<1>(acc, 1, partial);
-}
-
-static int ortho_blocks(int64_t n) {
-  int64_t b = (n + OT - 1) / OT;
-  int cap = g_ctx->num_sms * 3;
-  return (int)(b > cap ? cap : (b < 1 ? 1 : b));
-}
-static size_t ortho_smem() { return sizeof(double) * (32 * OT + OT); }
-static void ortho_attr() {
-  static bool done = false;
-  if (done) return;
-  MG_CUDA(cudaFuncSetAttribute(k_ortho<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ortho_smem()));
-  MG_CUDA(cudaFuncSetAttribute(k_ortho<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ortho_smem()));
-  done = true;
 }
 
 // u = sum y_k V_k (or u += when accumulate)
