@@ -248,11 +248,23 @@ def main():
     hbm, peak_kind = peaks()
     spmv_gbs = t.spmv_bytes * t.spmv_calls / (t.spmv_ms * 1e-3) / 1e9 if t.spmv_ms else None
     vc_gbs = t.vcycle_bytes * t.vcycle_calls / (t.vcycle_ms * 1e-3) / 1e9 if t.vcycle_ms else None
-    roofline = {"bound": "hbm", "kernel": "coarse-grid AMG V(2,2) cycle (L1-Jacobi CSR sweeps, R/P SpMV, "
-                                          "dense coarsest) on the MGR Schur operator",
-                "achieved": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": (vc_gbs / hbm) if vc_gbs else None,
-                "traffic": None, "peak_kind": peak_kind,
-                "bytes_per_launch": t.vcycle_bytes, "avg_launch_ms": t.vcycle_ms / max(t.vcycle_calls, 1)}
+    k0_gbs = t.k0_bytes * t.k0_calls / (t.k0_ms * 1e-3) / 1e9 if t.k0_ms else None
+    traffic = None
+    try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "k0_ncu.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        traffic = None
+    roofline = {"bound": "hbm", "kernel": "k_sell<4,EpiJacobi>: L1-Jacobi sweep (SELL-32 SpMV + fused update) on "
+                                          "the coarse-AMG level-0 operator (MGR Schur complement)",
+                "achieved": k0_gbs, "peak": hbm, "unit": "GB/s", "frac": (k0_gbs / hbm) if k0_gbs else None,
+                "traffic": traffic, "peak_kind": peak_kind, "bytes_per_launch": t.k0_bytes,
+                "avg_launch_ms": t.k0_ms / max(t.k0_calls, 1), "launches_timed": int(t.k0_calls)}
+    vc_roof = {"bound": "hbm", "kernel": "coarse-grid AMG V(2,2) cycle (composite: sweeps, residual, R/P, coarsest)",
+               "achieved": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": (vc_gbs / hbm) if vc_gbs else None,
+               "bytes_per_launch": t.vcycle_bytes, "avg_launch_ms": t.vcycle_ms / max(t.vcycle_calls, 1)}
+    phases = {nm: round(t.phase_ms[k], 3) for k, nm in enumerate(
+        ["bcsr_spmv", "coarse_amg", "f_relax_amg", "gmres_ortho", "mgr_transfers", "prescale", "d2h_sync"])}
     spmv_roof = {"bound": "hbm", "kernel": "BCSR b=2 SpMV (GMRES operator)", "achieved": spmv_gbs, "peak": hbm,
                  "unit": "GB/s", "frac": (spmv_gbs / hbm) if spmv_gbs else None,
                  "bytes_per_launch": t.spmv_bytes, "avg_launch_ms": t.spmv_ms / max(t.spmv_calls, 1)}
@@ -276,7 +288,8 @@ def main():
                            "parallelism": f"replicas x{ws}"},
                 "iterations": its[-1], "converged": conv, "setup_ms": statistics.median(setup_ms),
                 "solve_ms": statistics.median(solve_ms),
-                "roofline": roofline, "roofline_spmv": spmv_roof,
+                "roofline": roofline, "roofline_vcycle": vc_roof, "roofline_spmv": spmv_roof,
+                "solve_phase_ms": phases,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
         print(json.dumps(line), flush=True)
     rep.close()

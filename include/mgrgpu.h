@@ -195,6 +195,10 @@ typedef struct {
    * 0 BCSR SpMV, 1 coarse AMG cycles, 2 F-relaxation, 3 GMRES orthogonalisation,
    * 4 MGR level transfers / residuals, 5 prescale, 6 GMRES host sync + Givens, 7 other */
   double phase_ms[8];
+  /* the dominant single kernel: L1-Jacobi sweep on the coarse-AMG level-0 operator */
+  double k0_ms;
+  int64_t k0_calls;
+  double k0_bytes;       /* algorithmic bytes per launch */
 } mg_timing;
 int mg_get_timing(mg_ctx *ctx, mg_timing *t);
 /* CUDA-event timer on the context stream (bench timed regions) */

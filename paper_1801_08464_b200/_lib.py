@@ -44,7 +44,8 @@ class GmresRes(ctypes.Structure):
 class Timing(ctypes.Structure):
     _fields_ = [("setup_ms", c_double), ("solve_ms", c_double), ("spmv_ms", c_double),
                 ("spmv_calls", c_int64), ("vcycle_ms", c_double), ("vcycle_calls", c_int64),
-                ("vcycle_bytes", c_double), ("spmv_bytes", c_double), ("phase_ms", c_double * 8)]
+                ("vcycle_bytes", c_double), ("spmv_bytes", c_double), ("phase_ms", c_double * 8),
+                ("k0_ms", c_double), ("k0_calls", c_int64), ("k0_bytes", c_double)]
 
 
 _SIGS = {

@@ -481,6 +481,7 @@ static int gmres_common(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b
   g_ctx->timing.solve_ms = ms;
   g_ctx->timing.spmv_bytes = a->m.bytes_spmv();
   g_ctx->timing.vcycle_bytes = (m && m->h->camg) ? m->h->camg->cycle_bytes() : 0.0;
+  g_ctx->timing.k0_bytes = (m && m->h->camg) ? m->h->camg->k0_bytes() : 0.0;
   res->iterations = out.iterations;
   res->converged = out.converged;
   res->residual_norm = out.residual_norm;

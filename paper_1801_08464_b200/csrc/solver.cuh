@@ -28,7 +28,11 @@ struct Amg {
   bool has_sign = false;
   DBuf<double> cinv;      // dense inverse of the coarsest operator
   int cn = 0;
+  bool tag_k0 = false;    // time level-0 sweeps as the dominant kernel (MGR coarse AMG)
   double cycle_bytes() const;
+  double k0_bytes() const {  // L1-Jacobi sweep on level 0: SpMV + b, D^-1 (x own counted in gather)
+    return L.empty() ? 0.0 : L[0].A.bytes_spmv() + 16.0 * L[0].n;
+  }
 };
 
 std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o);
