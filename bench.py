@@ -224,9 +224,15 @@ def main():
     setup_ms, solve_ms = [], []
     ev = _Events(ctx)
     ev.record_start()
+    dbg = os.environ.get("BENCH_DEBUG") == "1"
     for _ in range(args.steps):
+        tw = time.perf_counter()
         device_step()
         t = ctx.timing()
+        if dbg:
+            ctx.sync()
+            print(f"step wall {1e3 * (time.perf_counter() - tw):.1f} ms setup {t.setup_ms:.1f} solve {t.solve_ms:.1f} "
+                  f"dev_bytes {ctx.device_bytes / 2**30:.2f} GiB", file=sys.stderr, flush=True)
         setup_ms.append(t.setup_ms)
         solve_ms.append(t.solve_ms)
         its.append(res.iterations)

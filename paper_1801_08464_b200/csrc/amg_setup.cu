@@ -84,8 +84,7 @@ bool sign_normalise(const Csr &a, Csr &out, DBuf<double> &sgn) {
   row_diag(a, d.p);
   sgn.alloc(n);
   DBuf<int> flags(2);
-  int init[2] = {0x7fffffff, 0};
-  h2d(flags.p, init, sizeof(init));
+  dset_i32(flags.p, {0x7fffffff, 0});
   if (n) {
     k_sign_of_diag<<<grid_for(n, 256), 256, 0, stream()>>>(n, d.p, sgn.p, flags.p);
     check_launch("sign_of_diag");
@@ -243,17 +242,20 @@ int pmis(const Csr &a, const int8_t *s, uint64_t seed, int level, DBuf<int8_t> &
   dzero(und.p, sizeof(int));
   k_pmis_init<<<grid_for(n, 256), 256, 0, stream()>>>(n, trp.p, seed, level, mu.p, state.p, und.p);
   check_launch("pmis_init");
-  int hu = 0;
-  d2h(&hu, und.p, sizeof(int));
+  // rounds are checked for termination in pairs (a round with nothing
+  // undecided is a no-op), halving the host round trips
+  int hu = 1;
   int rounds = 0;
   while (hu > 0) {
-    ++rounds;
-    k_pmis_select<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, trp.p, tind.p, mu.p, state.p,
-                                                           newc.p);
-    check_launch("pmis_select");
-    dzero(und.p, sizeof(int));
-    k_pmis_update<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, newc.p, state.p, und.p);
-    check_launch("pmis_update");
+    for (int pair = 0; pair < 2; ++pair) {
+      ++rounds;
+      k_pmis_select<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, trp.p, tind.p, mu.p,
+                                                             state.p, newc.p);
+      check_launch("pmis_select");
+      dzero(und.p, sizeof(int));
+      k_pmis_update<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, newc.p, state.p, und.p);
+      check_launch("pmis_update");
+    }
     d2h(&hu, und.p, sizeof(int));
     if (rounds > 100000) throw MgError(MG_ERR_AMG_SETUP, "PMIS did not terminate");
   }
@@ -640,8 +642,8 @@ Csr ext_interp(const Csr &a, const int8_t *s, const int8_t *state, const int *cm
   p.b = 1;
   p.rp.alloc((size_t)n + 1);
   DBuf<int> ub((size_t)(n ? n : 1)), cnt((size_t)(n ? n : 1)), ucnt((size_t)(n ? n : 1)), bad(1);
-  int big = 0x7fffffff;
-  h2d(bad.p, &big, sizeof(int));
+  const int big = 0x7fffffff;
+  dset_i32(bad.p, {big});
   if (n) {
     k_ext_ub<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, state, ub.p);
     check_launch("ext_ub");

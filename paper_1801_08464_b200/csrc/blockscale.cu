@@ -157,8 +157,8 @@ void block_scale(const Csr &a, Csr &dinv, Csr &ahat, bool equil) {
   k_diag_pattern<<<grid_for((int64_t)N + 1, 256), 256, 0, stream()>>>(N, dinv.rp.p, dinv.ci.p);
   check_launch("diag_pattern");
   DBuf<int> bad(1);
-  int big = 0x7fffffff;
-  h2d(bad.p, &big, sizeof(int));
+  const int big = 0x7fffffff;
+  dset_i32(bad.p, {big});
   if (B == 2)
     k_block_inv<2><<<grid_for(N, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, bad.p, eq);
   else

@@ -20,24 +20,37 @@ static size_t round_size(size_t b) {
   return (b + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1);
 }
 
+static Ctx *alloc_owner() { return g_ctx->owner ? g_ctx->owner : g_ctx; }
+
 void alloc_release_cache(Ctx *c) {
-  cudaStreamSynchronize(c->stream);
-  for (auto &kv : c->free_blocks) cudaFree(kv.second);
+  // caller holds c->amu (or no worker is running)
+  cudaDeviceSynchronize();
+  for (auto &pool : c->pools)
+    for (auto &kv : pool) cudaFree(kv.second.p);
+  for (auto &pool : c->pools) pool.clear();
   c->cached_bytes = 0;
-  c->free_blocks.clear();
 }
 
 void *dmalloc(size_t bytes) {
   if (!bytes) return nullptr;
-  Ctx *c = g_ctx;
+  Ctx *c = alloc_owner();
+  Ctx *me = g_ctx;
+  cudaStream_t s = me->stream;
+  std::lock_guard<std::mutex> lk(c->amu);
   size_t rb = round_size(bytes);
-  auto it = c->free_blocks.lower_bound(rb);
-  if (it != c->free_blocks.end() && it->first <= rb * 2 + ((size_t)4 << 20)) {
-    void *p = it->second;
+  const size_t limit = rb * 2 + ((size_t)4 << 20);
+  const bool worker = me->owner != nullptr;
+  if ((size_t)me->pool_id >= c->pools.size()) c->pools.resize(me->pool_id + 1);
+  auto &pool = c->pools[me->pool_id];
+  for (auto it = pool.lower_bound(rb); it != pool.end() && it->first <= limit; ++it) {
+    const Ctx::FreeBlk &fb = it->second;
+    bool ok = !fb.freer || fb.freer == s || (worker && fb.freer == c->stream && fb.epoch <= me->fork_epoch);
+    if (!ok) continue;
+    void *p = fb.p;
     size_t sz = it->first;
-    c->free_blocks.erase(it);
+    pool.erase(it);
     c->cached_bytes -= sz;
-    c->block_size[p] = sz;
+    c->block_size[p] = Ctx::BlkInfo{sz, me->pool_id};
     c->dev_bytes += (int64_t)sz;
     return p;
   }
@@ -53,7 +66,7 @@ void *dmalloc(size_t bytes) {
     throw MgError(MG_ERR_CUDA, std::string("device allocation of ") + std::to_string(bytes) +
                                    " bytes failed: " + cudaGetErrorString(e));
   }
-  c->block_size[p] = rb;
+  c->block_size[p] = Ctx::BlkInfo{rb, me->pool_id};
   c->dev_bytes += (int64_t)rb;
   return p;
 }
@@ -61,43 +74,196 @@ void *dmalloc(size_t bytes) {
 void dfree(void *p, size_t bytes) {
   (void)bytes;
   if (!p) return;
-  Ctx *c = g_ctx;
+  Ctx *c = alloc_owner();
+  std::lock_guard<std::mutex> lk(c->amu);
   auto it = c->block_size.find(p);
   if (it == c->block_size.end()) return;
-  size_t sz = it->second;
+  Ctx::BlkInfo bi = it->second;
   c->block_size.erase(it);
-  c->dev_bytes -= (int64_t)sz;
-  c->free_blocks.emplace(sz, p);
-  c->cached_bytes += sz;
+  c->dev_bytes -= (int64_t)bi.size;
+  if ((size_t)bi.home >= c->pools.size()) c->pools.resize(bi.home + 1);
+  c->pools[bi.home].emplace(bi.size, Ctx::FreeBlk{p, g_ctx->stream, c->epoch});
+  c->cached_bytes += bi.size;
 }
 
-void sync() { MG_CUDA(cudaStreamSynchronize(g_ctx->stream)); }
+// after a join (no worker running, their streams idle) every cached block is
+// safe on every stream: later workers fork behind the parent's work
+static void neutralise_all(Ctx *c) {
+  std::lock_guard<std::mutex> lk(c->amu);
+  for (auto &pool : c->pools)
+    for (auto &kv : pool) kv.second.freer = nullptr;
+}
 
-void trace(const char *what) {
+Ctx::~Ctx() {
+  for (auto &w : workers) {
+    if (!w) continue;
+    cudaStreamSynchronize(w->stream);
+    if (w->hbuf) cudaFreeHost(w->hbuf);
+    cudaStreamDestroy(w->stream);
+  }
+}
+
+TaskGroup::TaskGroup() : parent_(g_ctx) {}
+
+TaskGroup::~TaskGroup() {
+  if (!joined_) {
+    try { join(); } catch (...) {}
+  }
+}
+
+static bool concurrent_setup() {
   static int on = -1;
-  static std::chrono::steady_clock::time_point last;
+  if (on < 0) {
+    const char *e = getenv("MG_CONCURRENT_SETUP");
+    on = !(e && *e == '0');
+  }
+  return on;
+}
+
+void TaskGroup::run(std::function<void()> fn) {
+  if (!concurrent_setup() || trace_on()) {
+    fn();
+    return;
+  }
+  Ctx *p = parent_;
+  size_t k = used_.size();
+  if (k >= p->workers.size()) {
+    auto w = std::make_unique<Ctx>();
+    w->device = p->device;
+    w->num_sms = p->num_sms;
+    w->owner = p;
+    w->pool_id = (int)p->workers.size() + 1;
+    MG_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+    p->workers.push_back(std::move(w));
+  }
+  Ctx *w = p->workers[k].get();
+  w->launches = 0;
+  w->syncs = 0;
+  // the worker's stream starts after everything the parent enqueued so far,
+  // so blocks the parent freed before this point are safe on both streams
+  cudaEvent_t ev;
+  MG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  MG_CUDA(cudaEventRecord(ev, p->stream));
+  MG_CUDA(cudaStreamWaitEvent(w->stream, ev, 0));
+  cudaEventDestroy(ev);
+  {
+    std::lock_guard<std::mutex> lk(p->amu);
+    w->fork_epoch = p->epoch++;
+  }
+  used_.push_back(w);
+  err_.push_back(nullptr);
+  joined_ = false;
+  size_t slot = err_.size() - 1;
+  int dev = p->device;
+  th_.emplace_back([this, w, fn, slot, dev]() {
+    cudaSetDevice(dev);
+    g_ctx = w;
+    try {
+      fn();
+      sync();
+    } catch (...) {
+      err_[slot] = std::current_exception();
+      cudaStreamSynchronize(w->stream);
+    }
+    g_ctx = nullptr;
+  });
+}
+
+void TaskGroup::join() {
+  for (auto &t : th_)
+    if (t.joinable()) t.join();
+  th_.clear();
+  joined_ = true;
+  Ctx *p = parent_;
+  for (Ctx *w : used_) {
+    p->launches += w->launches;
+    p->syncs += w->syncs;
+  }
+  if (!used_.empty()) {
+    // worker streams are idle (each task synchronises its stream before its
+    // thread ends), so everything the parent enqueues from here on is ordered
+    // after the workers' work
+    neutralise_all(p);
+  }
+  used_.clear();
+  std::exception_ptr first = nullptr;
+  for (auto &e : err_)
+    if (e && !first) first = e;
+  err_.clear();
+  if (first) std::rethrow_exception(first);
+}
+
+void sync() {
+  g_ctx->syncs++;
+  MG_CUDA(cudaStreamSynchronize(g_ctx->stream));
+}
+
+bool trace_on() {
+  if (g_ctx && g_ctx->owner) return false;  // worker threads do not trace
+  static int on = -1;
   if (on < 0) {
     const char *e = getenv("MG_TRACE");
     on = e && *e && *e != '0';
-    last = std::chrono::steady_clock::now();
   }
-  if (!on) return;
+  return on;
+}
+
+void trace(const char *what) {
+  static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  static int64_t last_syncs = 0, last_launches = 0;
+  if (!trace_on()) return;
   sync();
+  int64_t ds = g_ctx->syncs - last_syncs, dl = g_ctx->launches - last_launches;
+  last_syncs = g_ctx->syncs;
+  last_launches = g_ctx->launches;
   auto now = std::chrono::steady_clock::now();
   double ms = std::chrono::duration<double, std::milli>(now - last).count();
-  fprintf(stderr, "[mg] %-40s %9.3f ms  (dev mem %.2f GiB)\n", what, ms, g_ctx->dev_bytes / 1073741824.0);
+  fprintf(stderr, "[mg] %-40s %9.3f ms  %4lld syncs %5lld launches (dev mem %.2f GiB)\n", what, ms,
+          (long long)ds, (long long)dl, g_ctx->dev_bytes / 1073741824.0);
   last = std::chrono::steady_clock::now();
 }
 
+// small transfers are staged through the context's pinned buffer (a pageable
+// copy goes through the driver's shared staging path and costs more per call)
+static const size_t STAGE_MAX = 64 << 10;
+
 void h2d(void *dst, const void *src, size_t bytes) {
   if (!bytes) return;
-  MG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_ctx->stream));
+  if (bytes <= STAGE_MAX) {
+    void *hs = host_scratch((bytes + 7) / 8);
+    memcpy(hs, src, bytes);
+    MG_CUDA(cudaMemcpyAsync(dst, hs, bytes, cudaMemcpyHostToDevice, g_ctx->stream));
+  } else {
+    MG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_ctx->stream));
+  }
   sync();
 }
 void d2h(void *dst, const void *src, size_t bytes) {
   if (!bytes) return;
+  if (bytes <= STAGE_MAX) {
+    void *hs = host_scratch((bytes + 7) / 8);
+    MG_CUDA(cudaMemcpyAsync(hs, src, bytes, cudaMemcpyDeviceToHost, g_ctx->stream));
+    sync();
+    memcpy(dst, hs, bytes);
+    return;
+  }
   MG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g_ctx->stream));
   sync();
+}
+
+struct I32x8 { int v[8]; };
+__global__ void k_set_i32(int *dst, I32x8 vals, int n) {
+  if (threadIdx.x < n) dst[threadIdx.x] = vals.v[threadIdx.x];
+}
+void dset_i32(int *dst, std::initializer_list<int> vals) {
+  I32x8 a{};
+  int n = 0;
+  for (int v : vals) {
+    if (n == 8) throw MgError(MG_ERR_BAD_OPTION, "dset_i32: at most 8 values");
+    a.v[n++] = v;
+  }
+  k_set_i32<<<1, 32, 0, g_ctx->stream>>>(dst, a, n);
+  check_launch("set_i32");
 }
 void dzero(void *dst, size_t bytes) {
   if (!bytes) return;

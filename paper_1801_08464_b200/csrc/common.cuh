@@ -2,8 +2,13 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <exception>
+#include <functional>
+#include <initializer_list>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -36,6 +41,7 @@ struct Ctx {
   std::string err;
   int64_t err_row = -1;
   int64_t launches = 0;
+  int64_t syncs = 0;      // host round trips (setup latency diagnostics)
   int64_t dev_bytes = 0;
   int num_sms = 148;
   int profiling = 0;
@@ -48,10 +54,46 @@ struct Ctx {
   void *cub_tmp = nullptr;
   size_t cub_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // mg_timer_start / mg_timer_stop
-  // caching allocator state (common.cu)
-  std::multimap<size_t, void *> free_blocks;
-  std::unordered_map<void *, size_t> block_size;
+  // caching allocator state (common.cu); owned by the API context, shared by
+  // its worker contexts under `amu`.  Every block has a home pool (the context
+  // that cudaMalloc'ed it: 0 = API context, k = worker k) and returns there
+  // when freed, so each context's pool converges to its own steady-state
+  // needs.  A free block also remembers the stream that freed it (nullptr =
+  // safe everywhere) and, for the parent stream, the fork epoch of the free:
+  // a worker may reuse a parent-freed block only if it was freed before the
+  // worker's fork (the worker's stream waits for that work); blocks freed by a
+  // worker are neutral only after the join.
+  struct FreeBlk { void *p; cudaStream_t freer; int64_t epoch; };
+  struct BlkInfo { size_t size; int home; };
+  std::vector<std::multimap<size_t, FreeBlk>> pools{1};
+  std::unordered_map<void *, BlkInfo> block_size;
   size_t cached_bytes = 0;
+  int pool_id = 0;          // this context's home pool
+  int64_t epoch = 0;        // parent: number of forks so far
+  int64_t fork_epoch = 0;   // worker: parent epoch at its fork
+  std::mutex amu;
+  // worker contexts (own stream + scratch) for concurrent setup tasks
+  Ctx *owner = nullptr;
+  std::vector<std::unique_ptr<Ctx>> workers;
+  ~Ctx();
+};
+
+// Concurrent setup tasks: each task runs on its own host thread with a worker
+// context (own stream, waits for the parent's work enqueued so far).  join()
+// waits for all of them, makes the parent stream ordered after them and
+// rethrows the first task error.
+class TaskGroup {
+ public:
+  TaskGroup();
+  ~TaskGroup();
+  void run(std::function<void()> fn);
+  void join();
+ private:
+  Ctx *parent_;
+  std::vector<std::thread> th_;
+  std::vector<Ctx *> used_;
+  std::vector<std::exception_ptr> err_;
+  bool joined_ = true;
 };
 
 void alloc_release_cache(Ctx *c);
@@ -152,11 +194,14 @@ inline int grid_for(int64_t work, int block, int max_blocks = 0) {
 
 // MG_TRACE=1: synchronise and print the wall time since the previous mark
 void trace(const char *what);
+bool trace_on();
 
 // host <-> device helpers (synchronous on the ctx stream)
 void h2d(void *dst, const void *src, size_t bytes);
 void d2h(void *dst, const void *src, size_t bytes);
 void dzero(void *dst, size_t bytes);
+// set up to 8 device ints from kernel parameters (stream-ordered, no host sync)
+void dset_i32(int *dst, std::initializer_list<int> vals);
 void d2d(void *dst, const void *src, size_t bytes);
 
 // scans / reductions (CUB)

@@ -146,8 +146,7 @@ int dense_inverse(const double *a_dev, double *inv_dev, int n) {
   if (n == 0) return -1;
   DBuf<double> aug((size_t)n * 2 * n);
   DBuf<int> flags(2);
-  int init[2] = {0, -1};
-  h2d(flags.p, init, sizeof(init));
+  dset_i32(flags.p, {0, -1});
   k_aug_init<<<grid_for((int64_t)n * 2 * n, 256, 4096), 256, 0, stream()>>>(a_dev, aug.p, n);
   check_launch("aug_init");
   if (n <= 256) {

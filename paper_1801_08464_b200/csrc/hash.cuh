@@ -5,8 +5,11 @@
 
 namespace mg {
 
+// Fibonacci hashing: the HIGH bits of k * 2^32/phi.  (The low bits of a
+// multiplicative hash depend only on the low bits of k, so stencil columns
+// spaced by powers of two -- +-nx, +-nx*ny -- would all collide.)
 __device__ __forceinline__ unsigned hash_k(int k, unsigned mask) {
-  return ((unsigned)k * 2654435761u) & mask;
+  return ((unsigned)k * 2654435769u) >> __clz((int)mask);
 }
 
 // insert key; returns 1 if newly inserted (keys[] initialised to -1)
@@ -55,6 +58,42 @@ __device__ __forceinline__ void warp_bitonic(int *L, int P, int lane) {
       }
       __syncwarp();
     }
+}
+
+// Register bitonic sort of a warp's 32*E elements, blocked layout (lane owns
+// elements lane*E .. lane*E+E-1), ascending; keys distinct except padding.
+template <int E, bool VAL = true>
+__device__ __forceinline__ void warp_sort_regs(int (&k)[E], int (&v)[E], int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (e & j) continue;
+          int m = lane * E + e;
+          bool asc = (m & size) == 0;
+          if ((k[e] > k[e ^ j]) == asc) {
+            int tk = k[e]; k[e] = k[e ^ j]; k[e ^ j] = tk;
+            if (VAL) { int tv = v[e]; v[e] = v[e ^ j]; v[e ^ j] = tv; }
+          }
+        }
+      } else {
+        const int lj = j / E;
+        bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          int m = lane * E + e;
+          bool asc = (m & size) == 0;
+          int ok = __shfl_xor_sync(0xffffffffu, k[e], lj);
+          int ov = VAL ? __shfl_xor_sync(0xffffffffu, v[e], lj) : 0;
+          bool take = (lower == asc) ? (ok < k[e]) : (ok > k[e]);
+          if (take) { k[e] = ok; if (VAL) v[e] = ov; }
+        }
+      }
+    }
+  }
 }
 
 struct WarpTables {
@@ -112,8 +151,47 @@ __device__ __forceinline__ void table_clear(WarpTables t, int T, int lane) {
   __syncwarp();
 }
 
+template <int E>
+__device__ __forceinline__ void table_sort_regs(WarpTables t, int T, int u, int lane) {
+  // compact (key, slot) pairs: keys into list, slots into the (not yet used) acc area
+  int *sl = (int *)t.acc;
+  int filled = 0;
+  for (int i0 = 0; i0 < T; i0 += 32) {
+    int k = t.keys[i0 + lane];
+    unsigned bal = __ballot_sync(0xffffffffu, k != -1);
+    if (k != -1) {
+      int p = filled + __popc(bal & ((1u << lane) - 1));
+      t.list[p] = k;
+      sl[p] = i0 + lane;
+    }
+    filled += __popc(bal);
+  }
+  __syncwarp();
+  int k[E], v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    int m = lane * E + e;
+    k[e] = m < u ? t.list[m] : 0x7fffffff;
+    v[e] = m < u ? sl[m] : -1;
+  }
+  __syncwarp();
+  warp_sort_regs<E>(k, v, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    int m = lane * E + e;
+    if (m < u) {
+      t.list[m] = k[e];
+      t.pos[v[e]] = m;
+    }
+  }
+  __syncwarp();
+}
+
 // gather the u inserted keys into list[0..u) sorted ascending; pos[slot] = rank
 __device__ __forceinline__ void table_sort(WarpTables t, int T, int u, int lane) {
+  if (u <= 32) { table_sort_regs<1>(t, T, u, lane); return; }
+  if (u <= 64) { table_sort_regs<2>(t, T, u, lane); return; }
+  if (u <= 128) { table_sort_regs<4>(t, T, u, lane); return; }
   unsigned mask = (unsigned)T - 1;
   int P = 32;
   while (P < u) P <<= 1;

@@ -216,8 +216,8 @@ void build_rp(const Csr &a, const int *fmap, const int *cmap, const int *flist, 
   DBuf<double> d(n);
   row_diag(a, d.p);
   DBuf<int> bad(1);
-  int big = 0x7fffffff;
-  h2d(bad.p, &big, sizeof(int));
+  const int big = 0x7fffffff;
+  dset_i32(bad.p, {big});
   k_fdiag_check<<<grid_for(nf, 256), 256, 0, stream()>>>(nf, flist, d.p, bad.p);
   check_launch("fdiag_check");
   int hb = 0;

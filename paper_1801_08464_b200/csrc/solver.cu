@@ -97,7 +97,11 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
   while (h->L.back().n > o.cutoff && (int)h->L.size() < o.max_levels) {
     int li = (int)h->L.size() - 1;
     AmgLevel &cur = h->L[li];
-    trace("amg level start");
+    if (trace_on()) {
+      char msg[96];
+      snprintf(msg, sizeof msg, "amg level %d start n=%d nnz=%lld", li, cur.n, (long long)cur.A.nnz);
+      trace(msg);
+    }
     DBuf<int8_t> s;
     if (strength(cur.A, o.theta, s) == 0) break;  // no strong connection: no progress
     trace("  strength");
@@ -348,8 +352,8 @@ static std::unique_ptr<BlockDiag> blockdiag_setup(const Csr &a, const std::vecto
   k_bd_gather<<<grid_for(nblk, 128), 128, 0, stream()>>>(nblk, k, bd->idx.p, a.rp.p, a.ci.p, a.v.p, blk.p);
   check_launch("bd_gather");
   DBuf<int> bad(1);
-  int big = 0x7fffffff;
-  h2d(bad.p, &big, sizeof(int));
+  const int big = 0x7fffffff;
+  dset_i32(bad.p, {big});
   k_bd_invert<<<grid_for(nblk, 64), 64, 0, stream()>>>(nblk, k, blk.p, bd->inv.p, bad.p);
   check_launch("bd_invert");
   int hb;
@@ -368,76 +372,94 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
   h->n0 = a.nr;
   h->post_smoothing = post_smoothing;
   h->coarse_kind = coarse_kind;
-  Csr cur = copy_csr(a);
-  // per-unknown owning cell, tracked down the levels only when a level relaxes globally
-  bool need_cells = false;
-  for (const LevelSpec &sp : plan) need_cells |= sp.global_relax != 0;
-  std::vector<int64_t> cells;
-  if (need_cells) {
-    cells.resize(a.nr);
-    for (int i = 0; i < a.nr; ++i) cells[i] = cells_host ? cells_host[i] : i;
-  }
-  for (const LevelSpec &sp : plan) {
-    int n = cur.nr;
-    if ((int)sp.fmask.size() != n) throw MgError(MG_ERR_DIM_MISMATCH, "level plan mask length mismatch");
-    int nf_h = 0;
-    for (uint8_t m : sp.fmask) nf_h += m != 0;
-    if (nf_h == 0 || nf_h == n) continue;
-    MgrLevel lv;
-    lv.n = n;
-    lv.rp = sp.rp;
-    DBuf<uint8_t> mask(n);
-    h2d(mask.p, sp.fmask.data(), n);
-    DBuf<int> cmap;
-    DBuf<int> &fmap = lv.fmap;
-    fc_split(mask.p, n, lv.flist, lv.clist, fmap, cmap, lv.nf, lv.nc);
-    trace("mgr: fc_split");
-    build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
-    trace("mgr: build_rp");
-    Csr ap = spgemm(cur, lv.P);
-    trace("mgr: A*P");
-    Csr ac = spgemm(lv.R, ap);
-    trace("mgr: R*(AP)");
-    lv.Aff = extract(cur, lv.flist.p, lv.nf, fmap.p, lv.nf);
-    trace("mgr: extract A_ff");
-    fsolver_setup(lv.fs, lv.Aff, sp, ao);
-    trace("mgr: F-solver setup");
-    if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
+  h->L.reserve(plan.size());
+  TaskGroup tasks;  // declared after h: joined before h can be destroyed
+  try {
+    Csr cur = copy_csr(a);
+    // per-unknown owning cell, tracked down the levels only when a level relaxes globally
+    bool need_cells = false;
+    for (const LevelSpec &sp : plan) need_cells |= sp.global_relax != 0;
+    std::vector<int64_t> cells;
     if (need_cells) {
-      std::vector<int64_t> nxt_cells(lv.nc);
-      std::vector<int> cl(lv.nc);
-      d2h(cl.data(), lv.clist.p, sizeof(int) * lv.nc);
-      for (int c = 0; c < lv.nc; ++c) nxt_cells[c] = cells[cl[c]];
-      cells.swap(nxt_cells);
+      cells.resize(a.nr);
+      for (int i = 0; i < a.nr; ++i) cells[i] = cells_host ? cells_host[i] : i;
     }
-    prepare_spmv(cur);
-    prepare_spmv(lv.R);
-    prepare_spmv(lv.P);
-    prepare_spmv(lv.Aff);
-    lv.res.alloc(n);
-    lv.rF.alloc(lv.nf);
-    lv.eF.alloc(lv.nf);
-    lv.rc.alloc(lv.nc);
-    lv.ec.alloc(lv.nc);
-    lv.A = std::move(cur);
-    cur = std::move(ac);
-    h->L.push_back(std::move(lv));
+    for (const LevelSpec &sp : plan) {
+      int n = cur.nr;
+      if ((int)sp.fmask.size() != n) throw MgError(MG_ERR_DIM_MISMATCH, "level plan mask length mismatch");
+      int nf_h = 0;
+      for (uint8_t m : sp.fmask) nf_h += m != 0;
+      if (nf_h == 0 || nf_h == n) continue;
+      MgrLevel lv;
+      lv.n = n;
+      lv.rp = sp.rp;
+      DBuf<uint8_t> mask(n);
+      h2d(mask.p, sp.fmask.data(), n);
+      DBuf<int> cmap;
+      DBuf<int> &fmap = lv.fmap;
+      fc_split(mask.p, n, lv.flist, lv.clist, fmap, cmap, lv.nf, lv.nc);
+      trace("mgr: fc_split");
+      build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
+      trace("mgr: build_rp");
+      Csr ap = spgemm(cur, lv.P);
+      trace("mgr: A*P");
+      Csr ac = spgemm(lv.R, ap);
+      trace("mgr: R*(AP)");
+      lv.Aff = extract(cur, lv.flist.p, lv.nf, fmap.p, lv.nf);
+      trace("mgr: extract A_ff");
+      if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
+      if (need_cells) {
+        std::vector<int64_t> nxt_cells(lv.nc);
+        std::vector<int> cl(lv.nc);
+        d2h(cl.data(), lv.clist.p, sizeof(int) * lv.nc);
+        for (int c = 0; c < lv.nc; ++c) nxt_cells[c] = cells[cl[c]];
+        cells.swap(nxt_cells);
+      }
+      prepare_spmv(cur);
+      prepare_spmv(lv.R);
+      prepare_spmv(lv.P);
+      lv.res.alloc(n);
+      lv.rF.alloc(lv.nf);
+      lv.eF.alloc(lv.nf);
+      lv.rc.alloc(lv.nc);
+      lv.ec.alloc(lv.nc);
+      lv.A = std::move(cur);
+      cur = std::move(ac);
+      h->L.push_back(std::move(lv));
+      // The F-relaxation setup (an AMG hierarchy on A_ff for FRelax('amg')) is
+      // independent of everything below this level: it runs concurrently on a
+      // worker stream while this thread builds the next level / coarse AMG.
+      MgrLevel *lvp = &h->L.back();  // stable: capacity reserved
+      const LevelSpec *spp = &sp;
+      tasks.run([lvp, spp, ao]() {
+        fsolver_setup(lvp->fs, lvp->Aff, *spp, ao);
+        prepare_spmv(lvp->Aff);
+        trace("mgr: F-solver setup");
+      });
+    }
+    trace("mgr: levels done");
+    if (coarse_kind == 0) {
+      h->camg = amg_setup(cur, ao);
+      h->camg->tag_k0 = true;
+      trace("mgr: coarse AMG setup");
+    } else {
+      if (cur.nr > DENSE_LIMIT) throw MgError(MG_ERR_UNSUPPORTED, "coarse='exact' on the GPU is limited to n <= 8192");
+      h->cn = cur.nr;
+      DBuf<double> dense((size_t)cur.nr * cur.nr);
+      to_dense(cur, dense.p);
+      h->cinv.alloc((size_t)cur.nr * cur.nr);
+      int bad = dense_inverse(dense.p, h->cinv.p, cur.nr);
+      if (bad >= 0) throw MgError(MG_ERR_SINGULAR, "coarse operator is singular", bad);
+    }
+    h->coarse_A = std::move(cur);
+  } catch (...) {
+    // a failing F-relaxation setup of an earlier level takes precedence (the
+    // reference reports errors in level order)
+    std::exception_ptr pe = std::current_exception();
+    tasks.join();
+    std::rethrow_exception(pe);
   }
-  trace("mgr: levels done");
-  if (coarse_kind == 0) {
-    h->camg = amg_setup(cur, ao);
-    h->camg->tag_k0 = true;
-    trace("mgr: coarse AMG setup");
-  } else {
-    if (cur.nr > DENSE_LIMIT) throw MgError(MG_ERR_UNSUPPORTED, "coarse='exact' on the GPU is limited to n <= 8192");
-    h->cn = cur.nr;
-    DBuf<double> dense((size_t)cur.nr * cur.nr);
-    to_dense(cur, dense.p);
-    h->cinv.alloc((size_t)cur.nr * cur.nr);
-    int bad = dense_inverse(dense.p, h->cinv.p, cur.nr);
-    if (bad >= 0) throw MgError(MG_ERR_SINGULAR, "coarse operator is singular", bad);
-  }
-  h->coarse_A = std::move(cur);
+  tasks.join();
   return h;
 }
 

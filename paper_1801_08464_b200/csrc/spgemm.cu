@@ -142,6 +142,32 @@ struct FillTabs {
   double *win;   // 32 window values
 };
 
+// register sort of the u <= 32E compacted keys in list, then write (key, acc)
+template <int E>
+__device__ __forceinline__ int emit_sorted(const FillTabs &t, unsigned mask, int u, int lane, int *oci,
+                                           double *ov) {
+  int k[E], d[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    int m = lane * E + e;
+    k[e] = m < u ? t.list[m] : 0x7fffffff;
+    d[e] = 0;
+  }
+  warp_sort_regs<E, false>(k, d, lane);
+  int nzc = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    int m = lane * E + e;
+    if (m < u) {
+      double val = t.acc[hash_find(t.keys, mask, k[e])];
+      oci[m] = k[e];
+      ov[m] = val;
+      nzc += val != 0.0;
+    }
+  }
+  return nzc;
+}
+
 __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, const int *arp, const int *aci,
                                          const double *av, const int *brp, const int *bci, const double *bv,
                                          const int64_t *base, int *oci, double *ov, int *nz) {
@@ -170,8 +196,6 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
     __syncwarp();
   });
   // sorted key list
-  int P = 32;
-  while (P < u) P <<= 1;
   int filled = 0;
   for (int i0 = 0; i0 < T; i0 += 32) {
     int k = t.keys[i0 + lane];
@@ -179,17 +203,25 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
     if (k != -1) t.list[filled + __popc(bal & ((1u << lane) - 1))] = k;
     filled += __popc(bal);
   }
-  for (int i = u + lane; i < P; i += 32) t.list[i] = 0x7fffffff;
   __syncwarp();
-  warp_bitonic(t.list, P, lane);
   int64_t o = base[row];
   int nzc = 0;
-  for (int q = lane; q < u; q += 32) {
-    int k = t.list[q];
-    double val = t.acc[hash_find(t.keys, mask, k)];
-    oci[o + q] = k;
-    ov[o + q] = val;
-    nzc += val != 0.0;
+  if (u <= 32) nzc = emit_sorted<1>(t, mask, u, lane, oci + o, ov + o);
+  else if (u <= 64) nzc = emit_sorted<2>(t, mask, u, lane, oci + o, ov + o);
+  else if (u <= 128) nzc = emit_sorted<4>(t, mask, u, lane, oci + o, ov + o);
+  else {
+    int P = 32;
+    while (P < u) P <<= 1;
+    for (int i = u + lane; i < P; i += 32) t.list[i] = 0x7fffffff;
+    __syncwarp();
+    warp_bitonic(t.list, P, lane);
+    for (int q = lane; q < u; q += 32) {
+      int k = t.list[q];
+      double val = t.acc[hash_find(t.keys, mask, k)];
+      oci[o + q] = k;
+      ov[o + q] = val;
+      nzc += val != 0.0;
+    }
   }
   for (int off = 16; off > 0; off >>= 1) nzc += __shfl_xor_sync(0xffffffffu, nzc, off);
   if (lane == 0) nz[row] = nzc;
@@ -319,6 +351,7 @@ void scale_i64(int64_t *a, int64_t s, int n) {
 }
 
 void RowBins::build(const int *ub_dev, int m, int layout) {
+  static_assert(NBIN + 1 == 8, "bin offsets are set from 8 kernel parameters");
   DBuf<int> bc(NBIN + 1);
   dzero(bc.p, sizeof(int) * (NBIN + 1));
   if (m) {
@@ -328,7 +361,7 @@ void RowBins::build(const int *ub_dev, int m, int layout) {
   d2h(cnt, bc.p, sizeof(int) * (NBIN + 1));
   off[0] = 0;
   for (int b = 1; b <= NBIN; ++b) off[b] = off[b - 1] + cnt[b - 1];
-  h2d(bc.p, off, sizeof(int) * (NBIN + 1));
+  dset_i32(bc.p, {off[0], off[1], off[2], off[3], off[4], off[5], off[6], off[7]});
   rows.alloc((size_t)(m ? m : 1));
   if (m) {
     k_bin_fill<<<grid_for(m, 256), 256, 0, stream()>>>(m, ub_dev, bc.p, rows.p);

@@ -137,14 +137,9 @@ def build_rp(a, part, kind):
     return DeviceMatrix(d.ctx, r), DeviceMatrix(d.ctx, p)
 
 
-def setup_from_matrix(a, level_plan, amg_opts=None, *, coarse="amg", post_smoothing=False,
-                      cells=None) -> MgrHierarchy:
-    """Generic MGR setup from (f_indices, spec) pairs (mgr.py:265-310), on the GPU."""
-    if coarse not in ("amg", "exact"):
-        raise ValueError(f"unknown coarse solver {coarse!r}")
-    d = as_device(a)
-    n0 = d.nrows
-    opts = as_options(amg_opts)
+def compile_plan(level_plan, n0: int):
+    """Host side of setup_from_matrix: (f_idx, spec) pairs -> per-level F masks,
+    C level specs and level dims.  Reusable across setups of the same plan."""
     specs, masks = [], []
     cur_n = n0
     dims = []
@@ -165,10 +160,37 @@ def setup_from_matrix(a, level_plan, amg_opts=None, *, coarse="amg", post_smooth
             cur_n -= nf
     dims.append(cur_n)
     arr = (_lib.LevelSpec * max(len(specs), 1))(*specs)
+    return CompiledPlan(n0, masks, arr, len(specs), dims)
+
+
+@dataclass
+class CompiledPlan:
+    n0: int
+    masks: list
+    specs: object
+    nspecs: int
+    dims: list
+
+
+def setup_from_matrix(a, level_plan, amg_opts=None, *, coarse="amg", post_smoothing=False,
+                      cells=None) -> MgrHierarchy:
+    """Generic MGR setup from (f_indices, spec) pairs (mgr.py:265-310), on the GPU.
+
+    ``level_plan`` may also be a ``CompiledPlan`` (``compile_plan``) to skip the
+    host-side mask construction when the same plan is set up repeatedly."""
+    if coarse not in ("amg", "exact"):
+        raise ValueError(f"unknown coarse solver {coarse!r}")
+    d = as_device(a)
+    n0 = d.nrows
+    opts = as_options(amg_opts)
+    cp = level_plan if isinstance(level_plan, CompiledPlan) else compile_plan(level_plan, n0)
+    if cp.n0 != n0:
+        raise ValueError("setup_from_matrix: plan compiled for a different dimension")
+    dims = cp.dims
     c_opts = opts.to_c()
     cells_arr = None if cells is None else _lib.i64(cells)
     h = _lib.P()
-    d.ctx.call("mg_mgr_setup", d.h, arr, len(specs), ctypes.byref(c_opts), 0 if coarse == "amg" else 1,
+    d.ctx.call("mg_mgr_setup", d.h, cp.specs, cp.nspecs, ctypes.byref(c_opts), 0 if coarse == "amg" else 1,
                int(bool(post_smoothing)), None if cells_arr is None else _lib.ptr(cells_arr), ctypes.byref(h))
     return MgrHierarchy(d.ctx, h, n0, dims, coarse, post_smoothing, a_ref=d)
 

@@ -21,7 +21,7 @@ import numpy as np
 from . import _lib
 from .amg import AmgOptions
 from .krylov import GmresOptions, GmresResult
-from .mgr import FRelax, MgrHierarchy, MgrLevelSpec, RpKind, setup_from_matrix
+from .mgr import FRelax, MgrHierarchy, MgrLevelSpec, RpKind, compile_plan, setup_from_matrix
 from .sparse import DeviceMatrix, block_scale
 
 # defaults used by bench.py, smoke() and the parity tests (oracle uses the same)
@@ -66,6 +66,7 @@ class SyntheticSolver:
         self.hier: MgrHierarchy | None = None
         self.dinv = None
         self.ahat = None
+        self._plan = None
 
     def upload(self, sysm) -> DeviceMatrix:
         self.sysm_meta = (sysm.b, sysm.n_cells)
@@ -83,8 +84,11 @@ class SyntheticSolver:
             if m is not None:
                 m.free()
         self.dinv, self.ahat = block_scale(a)
-        plan = default_plan(b, n_cells, self.rp, self.frelax)
-        self.hier = setup_from_matrix(self.ahat, plan, self.amg_opts)
+        key = (b, n_cells, a.nrows)
+        if self._plan is None or self._plan[0] != key:
+            # the plan is an input of the setup (fixed per system shape): built once
+            self._plan = (key, compile_plan(default_plan(b, n_cells, self.rp, self.frelax), a.nrows))
+        self.hier = setup_from_matrix(self.ahat, self._plan[1], self.amg_opts)
         self.hier.set_prescale(self.dinv)
         # Ahat is copied into the hierarchy; release the standalone copy
         self.ahat.free()
