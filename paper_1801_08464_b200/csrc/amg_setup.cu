@@ -305,23 +305,39 @@ struct ExtArgs {
 };
 
 // insert Chat_i = C^s_i u (C^s_k for strong-F k) into keys (initialised to -1);
-// returns |Chat_i| on every lane.  Lanes own consecutive entries of row i; for
-// strong-F k they walk row k (each lane its own k).
+// returns |Chat_i| on every lane.  Lanes own consecutive entries of row i; the
+// strong-F neighbours k of a 32-entry chunk are found with one ballot and the
+// whole warp walks each row k (coalesced 32-entry chunks).
 __device__ __forceinline__ int ext_candidates(int i, int *keys, unsigned mask, int lane, const ExtArgs &A) {
   const int *rp = A.rp, *ci = A.ci;
   const int8_t *s = A.s, *state = A.state;
   int b = rp[i], e = rp[i + 1];
   int mine = 0;
-  for (int q = b + lane; q < e; q += 32) {
-    int j = ci[q];
-    if (j == i || !s[q]) continue;
-    int sj = state[j];
-    if (sj == CPT) {
-      mine += hash_insert(keys, mask, j);
-    } else if (sj == FPT) {
-      for (int q2 = rp[j]; q2 < rp[j + 1]; ++q2) {
+  for (int q0 = b; q0 < e; q0 += 32) {
+    int q = q0 + lane;
+    int kk = -1, kb_l = 0, ke_l = 0;
+    if (q < e) {
+      int j = ci[q];
+      if (j != i && s[q]) {
+        int sj = state[j];
+        if (sj == CPT) {
+          mine += hash_insert(keys, mask, j);
+        } else if (sj == FPT) {
+          kk = j;
+          kb_l = rp[j];
+          ke_l = rp[j + 1];
+        }
+      }
+    }
+    unsigned km = __ballot_sync(0xffffffffu, kk >= 0);
+    while (km) {
+      int src = __ffs(km) - 1;
+      km &= km - 1;
+      int k = __shfl_sync(0xffffffffu, kk, src);
+      int kb = __shfl_sync(0xffffffffu, kb_l, src), ke = __shfl_sync(0xffffffffu, ke_l, src);
+      for (int q2 = kb + lane; q2 < ke; q2 += 32) {
         int l = ci[q2];
-        if (l != j && s[q2] && state[l] == CPT) mine += hash_insert(keys, mask, l);
+        if (l != k && s[q2] && state[l] == CPT) mine += hash_insert(keys, mask, l);
       }
     }
   }
