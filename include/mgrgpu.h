@@ -91,6 +91,17 @@ int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, int equilibrate, mg_mat **d
 /* z = G v (per-cell b x b matvec) */
 int mg_block_apply(mg_ctx *ctx, const mg_mat *dinv, const double *v, double *z);
 
+/* ---- GmresSolver system scaling (linsolve.py:94-122) ------------------------ */
+/* Symmetric infinity-norm equilibration (replaces GmresSolver._equilibrated,
+ * linsolve.py:107-122): *scaled_out = (diag(1/row) A) diag(col_scale), two
+ * rounded products per value with exact zeros dropped (scipy csr_matmat);
+ * row_out[n] = max_j |a_ij| (0 -> 1): divide the rhs by it; col_scale_out[n]
+ * = 1 / max_i |a_ij| / row_i (0 -> 1): multiply the solution by it.  Host
+ * output arrays. */
+int mg_equilibrate(mg_ctx *ctx, const mg_mat *a, mg_mat **scaled_out, double *row_out, double *col_scale_out);
+/* max_i sum_j |a_ij| of a scalar CSR matrix (the a_norm of linsolve.py:97-98) */
+int mg_abs_row_sum_max(mg_ctx *ctx, const mg_mat *a, double *out);
+
 /* ---- MGR build_rp (mgr.py:117-156) ------------------------------------------ */
 enum { MG_RP_INJECTIVE = 0, MG_RP_NONINJECTIVE = 1, MG_RP_INJECTION = 2, MG_RP_IDEAL = 3 };
 int mg_build_rp(mg_ctx *ctx, const mg_mat *a, const uint8_t *f_mask, int kind, mg_mat **r_out,

@@ -66,6 +66,8 @@ _SIGS = {
     "mg_extract": [P, P, P, c_int, P, c_int, ctypes.POINTER(P)],
     "mg_block_scale": [P, P, c_int, ctypes.POINTER(P), ctypes.POINTER(P)],
     "mg_block_apply": [P, P, P, P],
+    "mg_equilibrate": [P, P, ctypes.POINTER(P), P, P],
+    "mg_abs_row_sum_max": [P, P, ctypes.POINTER(c_double)],
     "mg_build_rp": [P, P, P, c_int, ctypes.POINTER(P), ctypes.POINTER(P)],
     "mg_amg_setup": [P, P, ctypes.POINTER(AmgOpts), ctypes.POINTER(P)],
     "mg_amg_vcycle": [P, P, P, P, P],

@@ -199,3 +199,121 @@ void block_apply(const Csr &dinv, const double *x, double *z) {
 }
 
 }  // namespace mg
+
+// ---- symmetric infinity-norm equilibration (GmresSolver._equilibrated) --------------
+// Replaces linsolve.py:107-122 (scipy):
+//   row = max_j |a_ij| (0 -> 1);  col = max_i (1/row_i) |a_ij| (0 -> 1)
+//   scaled = (diags(1/row) @ a) @ diags(1/col): each value ((1/row_i) a_ij) (1/col_j),
+//   two rounded products, exact zeros dropped after each product (csr_matmat)
+namespace mg {
+namespace {
+__global__ void k_row_absmax(int n, const int *rp, const double *v, double *row) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  double m = 0.0;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) m = fmax(m, fabs(v[q]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) row[wid] = m == 0.0 ? 1.0 : m;
+}
+__global__ void k_col_absmax(int n, const int *rp, const int *ci, const double *v, const double *row,
+                             unsigned long long *colbits) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  const double dr = __ddiv_rn(1.0, row[wid]);
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) {
+    double t = __dmul_rn(dr, fabs(v[q]));  // non-negative: bit order == value order
+    if (t > 0.0) atomicMax(colbits + ci[q], (unsigned long long)__double_as_longlong(t));
+  }
+}
+__global__ void k_col_scale(int n, const unsigned long long *colbits, double *colscale) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double c = __longlong_as_double((long long)colbits[j]);
+  colscale[j] = __ddiv_rn(1.0, c == 0.0 ? 1.0 : c);
+}
+__device__ __forceinline__ double eq_value(double a, double dr, double dc) {
+  double t = __dmul_rn(dr, a);
+  return t == 0.0 ? 0.0 : __dmul_rn(t, dc);
+}
+__global__ void k_eq_count(int n, const int *rp, const int *ci, const double *v, const double *row,
+                           const double *colscale, int *cnt) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  const double dr = __ddiv_rn(1.0, row[wid]);
+  int c = 0;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) c += eq_value(v[q], dr, colscale[ci[q]]) != 0.0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[wid] = c;
+}
+__global__ void k_eq_fill(int n, const int *rp, const int *ci, const double *v, const double *row,
+                          const double *colscale, const int *orp, int *oci, double *ov) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  const double dr = __ddiv_rn(1.0, row[wid]);
+  int o = orp[wid];
+  for (int q0 = rp[wid]; q0 < rp[wid + 1]; q0 += 32) {
+    int q = q0 + lane;
+    double val = q < rp[wid + 1] ? eq_value(v[q], dr, colscale[ci[q]]) : 0.0;
+    unsigned bal = __ballot_sync(0xffffffffu, val != 0.0);
+    if (val != 0.0) {
+      int p = o + __popc(bal & ((1u << lane) - 1));
+      oci[p] = ci[q];
+      ov[p] = val;
+    }
+    o += __popc(bal);
+  }
+}
+__global__ void k_abs_row_sum_max(int n, const int *rp, const double *v, unsigned long long *out) {
+  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n) return;
+  double s = 0.0;
+  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) s += fabs(v[q]);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0 && s > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(s));
+}
+}  // namespace
+
+void equilibrate(const Csr &a, Csr &out, double *row_dev, double *colscale_dev) {
+  if (a.b != 1 || a.nr != a.nc) throw MgError(MG_ERR_UNSUPPORTED, "equilibrate: square scalar CSR required");
+  const int n = a.nr;
+  out.nr = out.nc = n;
+  out.b = 1;
+  out.rp.alloc((size_t)n + 1);
+  if (!n) {
+    dzero(out.rp.p, sizeof(int));
+    return;
+  }
+  const int g = grid_for((int64_t)n * 32, 256);
+  k_row_absmax<<<g, 256, 0, stream()>>>(n, a.rp.p, a.v.p, row_dev);
+  check_launch("row_absmax");
+  DBuf<unsigned long long> colbits(n);
+  dzero(colbits.p, sizeof(unsigned long long) * n);
+  k_col_absmax<<<g, 256, 0, stream()>>>(n, a.rp.p, a.ci.p, a.v.p, row_dev, colbits.p);
+  check_launch("col_absmax");
+  k_col_scale<<<grid_for(n, 256), 256, 0, stream()>>>(n, colbits.p, colscale_dev);
+  check_launch("col_scale");
+  DBuf<int> cnt(n);
+  k_eq_count<<<g, 256, 0, stream()>>>(n, a.rp.p, a.ci.p, a.v.p, row_dev, colscale_dev, cnt.p);
+  check_launch("eq_count");
+  out.nnz = exclusive_scan_i32_to_i32(cnt.p, out.rp.p, n);
+  out.ci.alloc((size_t)out.nnz);
+  out.v.alloc((size_t)out.nnz);
+  k_eq_fill<<<g, 256, 0, stream()>>>(n, a.rp.p, a.ci.p, a.v.p, row_dev, colscale_dev, out.rp.p, out.ci.p,
+                                     out.v.p);
+  check_launch("eq_fill");
+}
+
+double abs_row_sum_max(const Csr &a) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "abs_row_sum_max: scalar CSR required");
+  if (!a.nr) return 0.0;
+  DBuf<unsigned long long> m(1);
+  dzero(m.p, sizeof(unsigned long long));
+  k_abs_row_sum_max<<<grid_for((int64_t)a.nr * 32, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.v.p, m.p);
+  check_launch("abs_row_sum_max");
+  unsigned long long h = 0;
+  d2h(&h, m.p, sizeof(h));
+  double r;
+  memcpy(&r, &h, sizeof(r));
+  return r;
+}
+}  // namespace mg

@@ -5,4 +5,10 @@ namespace mg {
 // dinv: block-diagonal BSR (N blocks); ahat: scalar CSR cell-major
 void block_scale(const Csr &a, Csr &dinv, Csr &ahat, bool equilibrate);
 void block_apply(const Csr &dinv, const double *x, double *z);
+// symmetric infinity-norm equilibration (linsolve.py:107-122): row = row abs max
+// (0 -> 1), colscale = 1 / col abs max of diag(1/row)|A| (0 -> 1), out = the
+// scaled matrix with exact zeros dropped
+void equilibrate(const Csr &a, Csr &out, double *row_dev, double *colscale_dev);
+// max_i sum_j |a_ij|  (the a_norm GmresSolver passes to gmres, linsolve.py:98)
+double abs_row_sum_max(const Csr &a);
 }  // namespace mg

@@ -253,6 +253,23 @@ int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, int equilibrate, mg_mat **d
   });
 }
 
+int mg_equilibrate(mg_ctx *ctx, const mg_mat *a, mg_mat **scaled_out, double *row_out, double *col_scale_out) {
+  return guard(ctx, [&] {
+    if (a->m.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "equilibrate: scalar CSR required");
+    int n = a->m.nr;
+    DBuf<double> row((size_t)(n ? n : 1)), cs((size_t)(n ? n : 1));
+    auto o = std::make_unique<mg_mat>();
+    equilibrate(a->m, o->m, row.p, cs.p);
+    if (row_out) d2h(row_out, row.p, sizeof(double) * n);
+    if (col_scale_out) d2h(col_scale_out, cs.p, sizeof(double) * n);
+    *scaled_out = o.release();
+  });
+}
+
+int mg_abs_row_sum_max(mg_ctx *ctx, const mg_mat *a, double *out) {
+  return guard(ctx, [&] { *out = abs_row_sum_max(a->m); });
+}
+
 int mg_block_apply(mg_ctx *ctx, const mg_mat *dinv, const double *v, double *z) {
   return guard(ctx, [&] {
     int64_t n = vec_len(dinv->m);

@@ -249,7 +249,8 @@ static void fsolver_setup(FSolver &fs, Csr &aff, const LevelSpec &sp, const AmgO
     int bad = dense_inverse(dense.p, fs.dinv.p, aff.nr);
     if (bad >= 0) throw MgError(MG_ERR_SINGULAR, "A_ff is singular", bad);
   } else {
-    throw MgError(MG_ERR_UNSUPPORTED, "FRelax('gauss_seidel') is not available on the GPU path");
+    tril_setup(aff, fs.tril);
+    fs.ctrl.alloc(nf + 1);
   }
 }
 
@@ -264,44 +265,59 @@ static void fsolve(FSolver &fs, const Csr &aff, const double *r, double *x) {
     if (cur != x) vcopy(x, cur, fs.nf);
   } else if (fs.kind == FR_AMG) {
     amg_vcycle(*fs.amg, r, nullptr, x);
+  } else if (fs.kind == FR_GS) {
+    // x = L^-1 r; x += L^-1 (r - A_ff x) per further sweep (mgr.py:185-188)
+    trsv_lower(fs.tril, r, x, fs.ctrl.p);
+    for (int s = 1; s < fs.sweeps; ++s) {
+      residual(aff, x, r, fs.t1.p);
+      trsv_lower(fs.tril, fs.t1.p, fs.t2.p, fs.ctrl.p);
+      vadd(x, fs.t2.p, fs.nf);
+    }
   } else {
     dense_matvec(fs.dinv.p, r, x, fs.nf);
   }
 }
 
-// per-cell block-diagonal relaxation (uniform block size)
-__global__ void k_bd_apply(int nblk, int k, const int *idx, const double *inv, const double *r, double *x) {
+// per-cell block-diagonal relaxation: x[id] = inv_b r[id] per block
+__global__ void k_bd_apply(int nblk, const int *ioff, const int64_t *moff, const int *idx, const double *inv,
+                           const double *r, double *x) {
   int bi = blockIdx.x * blockDim.x + threadIdx.x;
   if (bi >= nblk) return;
-  const int *id = idx + (int64_t)bi * k;
-  const double *m = inv + (int64_t)bi * k * k;
+  const int k = ioff[bi + 1] - ioff[bi];
+  const int *id = idx + ioff[bi];
+  const double *m = inv + moff[bi];
   for (int a = 0; a < k; ++a) {
     double s = 0.0;
     for (int c = 0; c < k; ++c) s += m[a * k + c] * r[id[c]];
     x[id[a]] = s;
   }
 }
-__global__ void k_bd_gather(int nblk, int k, const int *idx, const int *rp, const int *ci, const double *v,
-                            double *blk) {
+__global__ void k_bd_gather(int nblk, const int *ioff, const int64_t *moff, const int *idx, const int *rp,
+                            const int *ci, const double *v, double *blk) {
   int bi = blockIdx.x * blockDim.x + threadIdx.x;
   if (bi >= nblk) return;
-  const int *id = idx + (int64_t)bi * k;
+  const int k = ioff[bi + 1] - ioff[bi];
+  const int *id = idx + ioff[bi];
+  double *o = blk + moff[bi];
   for (int a = 0; a < k; ++a)
     for (int c = 0; c < k; ++c) {
       double val = 0.0;
       int row = id[a], col = id[c];
       for (int q = rp[row]; q < rp[row + 1]; ++q)
         if (ci[q] == col) { val = v[q]; break; }
-      blk[((int64_t)bi * k + a) * k + c] = val;
+      o[a * k + c] = val;
     }
 }
 // small dense inverses by Gauss-Jordan with partial pivoting, one thread per block (k <= 8)
-__global__ void k_bd_invert(int nblk, int k, double *blk, double *inv, int *bad) {
+__global__ void k_bd_invert(int nblk, const int *ioff, const int64_t *moff, const double *blk, double *inv,
+                            int *bad) {
   int bi = blockIdx.x * blockDim.x + threadIdx.x;
   if (bi >= nblk) return;
+  const int k = ioff[bi + 1] - ioff[bi];
+  const double *bk = blk + moff[bi];
   double a[8][16];
   for (int i = 0; i < k; ++i)
-    for (int j = 0; j < 2 * k; ++j) a[i][j] = j < k ? blk[((int64_t)bi * k + i) * k + j] : (j - k == i ? 1.0 : 0.0);
+    for (int j = 0; j < 2 * k; ++j) a[i][j] = j < k ? bk[i * k + j] : (j - k == i ? 1.0 : 0.0);
   for (int c = 0; c < k; ++c) {
     int p = c;
     for (int i = c + 1; i < k; ++i)
@@ -318,44 +334,58 @@ __global__ void k_bd_invert(int nblk, int k, double *blk, double *inv, int *bad)
         for (int j = 0; j < 2 * k; ++j) a[i][j] -= f * a[c][j];
     }
   }
+  double *o = inv + moff[bi];
   for (int i = 0; i < k; ++i)
-    for (int j = 0; j < k; ++j) inv[((int64_t)bi * k + i) * k + j] = a[i][k + j];
+    for (int j = 0; j < k; ++j) o[i * k + j] = a[i][k + j];
 }
 
 static std::unique_ptr<BlockDiag> blockdiag_setup(const Csr &a, const std::vector<int64_t> &cells) {
-  // group unknowns by owning cell (stable), all groups must share one size
+  // group unknowns by owning cell (stable sort of cells, mgr.py:219-224);
+  // each group is one dense block (sizes may differ between cells)
   int n = a.nr;
   std::vector<int> order(n);
   for (int i = 0; i < n; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cells[x] < cells[y]; });
-  std::vector<int> idx;
-  int k = -1, nblk = 0;
+  std::vector<int> idx, ioff{0};
+  std::vector<int64_t> moff{0};
+  int kmax = 0;
   for (int s = 0; s < n;) {
     int e = s;
     while (e < n && cells[order[e]] == cells[order[s]]) ++e;
     std::vector<int> g(order.begin() + s, order.begin() + e);
     std::sort(g.begin(), g.end());
-    if (k < 0) k = (int)g.size();
-    if ((int)g.size() != k) throw MgError(MG_ERR_UNSUPPORTED, "global_relax: mixed per-cell block sizes");
+    int k = (int)g.size();
+    if (k > 8) throw MgError(MG_ERR_UNSUPPORTED, "global_relax: per-cell blocks larger than 8");
+    kmax = std::max(kmax, k);
     idx.insert(idx.end(), g.begin(), g.end());
-    ++nblk;
+    ioff.push_back((int)idx.size());
+    moff.push_back(moff.back() + (int64_t)k * k);
     s = e;
   }
-  if (k > 8) throw MgError(MG_ERR_UNSUPPORTED, "global_relax: per-cell blocks larger than 8");
   auto bd = std::make_unique<BlockDiag>();
-  bd->nblk = nblk;
-  bd->k = k;
+  bd->nblk = (int)ioff.size() - 1;
+  bd->kmax = kmax;
   bd->idx.alloc(idx.size());
   h2d(bd->idx.p, idx.data(), sizeof(int) * idx.size());
-  DBuf<double> blk((size_t)nblk * k * k);
-  bd->inv.alloc((size_t)nblk * k * k);
-  k_bd_gather<<<grid_for(nblk, 128), 128, 0, stream()>>>(nblk, k, bd->idx.p, a.rp.p, a.ci.p, a.v.p, blk.p);
-  check_launch("bd_gather");
+  bd->ioff.alloc(ioff.size());
+  h2d(bd->ioff.p, ioff.data(), sizeof(int) * ioff.size());
+  bd->moff.alloc(moff.size());
+  h2d(bd->moff.p, moff.data(), sizeof(int64_t) * moff.size());
+  const int nblk = bd->nblk;
+  DBuf<double> blk((size_t)(moff.back() ? moff.back() : 1));
+  bd->inv.alloc((size_t)(moff.back() ? moff.back() : 1));
+  if (nblk) {
+    k_bd_gather<<<grid_for(nblk, 128), 128, 0, stream()>>>(nblk, bd->ioff.p, bd->moff.p, bd->idx.p, a.rp.p,
+                                                           a.ci.p, a.v.p, blk.p);
+    check_launch("bd_gather");
+  }
   DBuf<int> bad(1);
   const int big = 0x7fffffff;
   dset_i32(bad.p, {big});
-  k_bd_invert<<<grid_for(nblk, 64), 64, 0, stream()>>>(nblk, k, blk.p, bd->inv.p, bad.p);
-  check_launch("bd_invert");
+  if (nblk) {
+    k_bd_invert<<<grid_for(nblk, 64), 64, 0, stream()>>>(nblk, bd->ioff.p, bd->moff.p, blk.p, bd->inv.p, bad.p);
+    check_launch("bd_invert");
+  }
   int hb;
   d2h(&hb, bad.p, sizeof(int));
   if (hb != big) throw MgError(MG_ERR_SINGULAR, "singular per-cell block", hb);
@@ -472,8 +502,8 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
   MgrLevel &lv = h.L[k];
   bool zero = true;
   if (lv.bd) {
-    k_bd_apply<<<grid_for(lv.bd->nblk, 128), 128, 0, stream()>>>(lv.bd->nblk, lv.bd->k, lv.bd->idx.p,
-                                                                 lv.bd->inv.p, r, e);
+    k_bd_apply<<<grid_for(lv.bd->nblk, 128), 128, 0, stream()>>>(lv.bd->nblk, lv.bd->ioff.p, lv.bd->moff.p,
+                                                                 lv.bd->idx.p, lv.bd->inv.p, r, e);
     check_launch("bd_apply");
     zero = false;
   }

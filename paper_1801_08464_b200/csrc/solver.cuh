@@ -51,6 +51,8 @@ struct LevelSpec {
 struct FSolver {
   int kind = FR_JACOBI, sweeps = 1;
   DBuf<double> invd;           // jacobi
+  Csr tril;                    // gauss_seidel: lower triangle of A_ff (diagonal last)
+  DBuf<int> ctrl;              // gauss_seidel: substitution ticket + ready flags
   std::unique_ptr<Amg> amg;    // amg
   DBuf<double> dinv;           // exact (dense inverse)
   DBuf<double> t1, t2;
@@ -58,9 +60,11 @@ struct FSolver {
 };
 
 struct BlockDiag {             // per-cell block-diagonal relaxation (mgr.py:212-242)
-  int nblk = 0, k = 0;         // uniform block size k
-  DBuf<int> idx;               // nblk * k unknowns
-  DBuf<double> inv;            // nblk * k * k
+  int nblk = 0, kmax = 0;      // blocks of size ioff[b+1]-ioff[b] <= 8 (mixed sizes allowed)
+  DBuf<int> idx;               // unknowns of all blocks, concatenated
+  DBuf<int> ioff;              // nblk + 1 offsets into idx
+  DBuf<int64_t> moff;          // nblk + 1 offsets into inv (k*k per block)
+  DBuf<double> inv;            // row-major block inverses
 };
 
 struct MgrLevel {
@@ -112,6 +116,10 @@ void fc_split(const uint8_t *fmask_dev, int n, DBuf<int> &flist, DBuf<int> &clis
               DBuf<int> &cmap, int &nf, int &nc);
 void build_rp(const Csr &a, const int *fmap, const int *cmap, const int *flist, const int *clist, int nf,
               int nc, int kind, Csr &r, Csr &p);
+
+// Gauss-Seidel F-relaxation (trisolve.cu)
+void tril_setup(const Csr &a, Csr &l);
+void trsv_lower(const Csr &l, const double *r, double *x, int *ctrl);
 
 // profiling of the hot kernels inside a solve
 struct ProfScope {

@@ -12,9 +12,14 @@ are accepted too (duck-typed by field names / enum value).
 Deviation (SURVEY.md §7 hard part viii, mirrored by oracle/mgr.py): the
 F-relaxation AMG keeps every AmgOptions field except those FRelax overrides
 (the reference's _AmgF drops ``interpolation``, mgr.py:193-197).
-Not available on the GPU: FRelax('gauss_seidel') (sequential triangular
-solve) raises UnsupportedOnGpu; 'exact' / IDEAL / coarse='exact' use dense
-inverses and are limited to 8192 unknowns.
+FRelax('gauss_seidel') runs a sync-free forward substitution with tril(A_ff)
+on the device (csrc/trisolve.cu; the reference uses SuperLU, mgr.py:175-188).
+'exact' / IDEAL / coarse='exact' and a coarsest AMG level use dense inverses
+and are limited to 8192 unknowns.
+
+The label-based ``mgr_setup(system, specs)`` (mgr.py:313-333) and the scenario
+presets ``default_2p2c_specs`` / ``cpr_specs`` (mgr.py:380-427) are mirrored
+for the physics drop-in (``linsolve.GmresSolver``).
 """
 from __future__ import annotations
 
@@ -203,3 +208,61 @@ def mgr_apply(hier: MgrHierarchy, r) -> np.ndarray:
     e = np.empty(hier.n)
     hier.ctx.call("mg_mgr_apply", hier.h, _lib.ptr(r), _lib.ptr(e))
     return e
+
+
+# -- label-based setup and scenario presets (mgr.py:313-333, 380-427) ---------
+# unknown labels of a BlockSystem (assembly.py:32-35)
+LABEL_P, LABEL_S, LABEL_RHO_ACTIVE, LABEL_RHO_INACTIVE = 0, 1, 2, 3
+ACTIVE_CONSTRAINTS = (LABEL_RHO_ACTIVE,)
+SATURATIONS = (LABEL_S,)
+INACTIVE_CONSTRAINTS = (LABEL_RHO_INACTIVE,)
+NON_PRESSURE = (LABEL_S, LABEL_RHO_ACTIVE, LABEL_RHO_INACTIVE)
+
+
+def label_plan(labels, specs):
+    """(f_idx, spec) pairs from unknown labels (mgr.py:322-331): each spec takes the
+    current level's unknowns whose label is in ``spec.f_labels``; the labels of
+    surviving C points carry down, and a spec matching nothing (or everything)
+    is kept in the plan and skipped by the setup."""
+    plan = []
+    remaining = np.asarray(labels)
+    for spec in specs:
+        f_idx = np.where(np.isin(remaining, spec.f_labels))[0]
+        plan.append((f_idx, spec))
+        if 0 < f_idx.size < remaining.size:
+            keep = np.ones(remaining.size, dtype=bool)
+            keep[f_idx] = False
+            remaining = remaining[keep]
+    return plan
+
+
+def mgr_setup(system, specs, amg_opts=None, *, coarse="amg", post_smoothing=False) -> MgrHierarchy:
+    """Reduction hierarchy for a two-phase NCP block system (mgr.py:313-333).
+
+    ``system`` is duck-typed like ncpflow's BlockSystem: ``.a`` (CsrMatrix,
+    scipy sparse or DeviceMatrix), ``.labels()`` and ``.cells()``."""
+    plan = label_plan(system.labels(), specs)
+    return setup_from_matrix(system.a, plan, amg_opts, coarse=coarse, post_smoothing=post_smoothing,
+                             cells=system.cells())
+
+
+def default_2p2c_specs(scenario_kind: str):
+    """Per-scenario reduction configuration (mgr.py:388-416), same data."""
+    if scenario_kind == "unsaturated":
+        return [
+            MgrLevelSpec(ACTIVE_CONSTRAINTS, RpKind.INJECTIVE, FRelax("gauss_seidel", sweeps=3)),
+            MgrLevelSpec(SATURATIONS, RpKind.INJECTIVE, FRelax("amg", pre=0, post=1)),
+        ]
+    if scenario_kind in ("gas_appearance", "box3d"):
+        return [
+            MgrLevelSpec(ACTIVE_CONSTRAINTS, RpKind.NONINJECTIVE, FRelax("jacobi", sweeps=1)),
+            MgrLevelSpec(SATURATIONS, RpKind.NONINJECTIVE, FRelax("amg", pre=1, post=1, max_levels=2)),
+            MgrLevelSpec(INACTIVE_CONSTRAINTS, RpKind.NONINJECTIVE, FRelax("amg", pre=1, post=1, max_levels=2)),
+        ]
+    raise ValueError(f"no default MGR configuration for scenario {scenario_kind!r}")
+
+
+def cpr_specs(gs_sweeps: int = 1):
+    """CPR-AMG emulation (mgr.py:419-427): every non-pressure unknown an F point,
+    pure injection transfers, Gauss-Seidel F-relaxation."""
+    return [MgrLevelSpec(NON_PRESSURE, RpKind.INJECTION, FRelax("gauss_seidel", sweeps=gs_sweeps))]

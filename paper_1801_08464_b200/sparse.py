@@ -208,3 +208,24 @@ def block_apply(dinv: DeviceMatrix, v) -> np.ndarray:
     z = np.empty_like(v)
     dinv.ctx.call("mg_block_apply", dinv.h, _lib.ptr(v), _lib.ptr(z))
     return z
+
+
+def equilibrate(a: DeviceMatrix):
+    """Symmetric infinity-norm equilibration on the device (linsolve.py:107-122).
+
+    Returns (scaled DeviceMatrix, row, col_scale): scaled = (diag(1/row) A) diag(col_scale)
+    with exact zeros dropped; divide the rhs by ``row``, multiply the solution by
+    ``col_scale``."""
+    n = a.nrows
+    row = np.empty(n)
+    col = np.empty(n)
+    h = _lib.P()
+    a.ctx.call("mg_equilibrate", a.h, _lib.ctypes.byref(h), _lib.ptr(row), _lib.ptr(col))
+    return DeviceMatrix(a.ctx, h), row, col
+
+
+def abs_row_sum_max(a: DeviceMatrix) -> float:
+    """max_i sum_j |a_ij| (the ``a_norm`` GmresSolver passes to gmres, linsolve.py:97-98)."""
+    out = _lib.ctypes.c_double()
+    a.ctx.call("mg_abs_row_sum_max", a.h, _lib.ctypes.byref(out))
+    return float(out.value)
