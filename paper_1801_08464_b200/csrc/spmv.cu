@@ -131,7 +131,12 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   // short rows (where CSR lane groups are inefficient), 1.15x otherwise
   // (measured: irregular long-row coarse levels lose with SELL)
   double avg = (double)a.nnz / (a.nr ? a.nr : 1);
-  double cap = avg <= 16.0 ? 2.0 : 1.15;
+  static double cap_long = -1.0;
+  if (cap_long < 0) {
+    const char *e = getenv("MG_SELL_CAP_LONG");
+    cap_long = e ? atof(e) : 1.15;
+  }
+  double cap = avg <= 16.0 ? 2.0 : cap_long;
   if (padded > (int64_t)(cap * (double)a.nnz) + 4096 || padded > 2000000000LL) {
     pl.rlen.release();
     return;
@@ -200,7 +205,7 @@ void prepare_spmv(const Csr &a) {
       k_cls_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, cnt.p, pl->rows.p);
       check_launch("cls_fill");
     }
-    if (a.nr >= 32768 && a.nnz >= 4 * (int64_t)a.nr) build_sell(a, *pl);
+    if (a.nr >= 32768 && a.nnz >= 3 * (int64_t)a.nr) build_sell(a, *pl);
   }
   a.plan = std::move(pl);
 }
@@ -324,9 +329,12 @@ static void launch_csr(const Csr &a, const double *x, Epi epi) {
     else if (avg <= 5) LAUNCH_AVG(4, 2);
     else if (avg <= 9) LAUNCH_AVG(4, 3);
     else if (avg <= 18) LAUNCH_AVG(8, 3);
-    else if (avg <= 36) LAUNCH_AVG(16, 3);
-    else if (avg <= 72) LAUNCH_AVG(16, 5);
-    else LAUNCH_AVG(32, 4);
+    // measured on the config-3 hierarchies (tools/kbench.py): 8 lanes x 2 for
+    // ~26/row (F-relax A_1, 58 -> 68% of HBM), 8 x 4 for ~40-60/row, 16 x 4
+    // for the ~100-150/row coarse-AMG levels (76 -> 84%)
+    else if (avg <= 36) LAUNCH_AVG(8, 2);
+    else if (avg <= 72) LAUNCH_AVG(8, 4);
+    else LAUNCH_AVG(16, 4);
     check_launch("csr spmv");
     return;
   }

@@ -56,8 +56,13 @@ def main():
     rows.append(("MGR P", h.level_matrix(0, "p")))
     rows.append(("MGR A_ff", h.level_matrix(0, "a_ff")))
     camg = h.amg(-1)
-    for k in range(min(3, camg.nlevels)):
-        rows.append((f"coarse AMG A_{k}", camg.levels[k].a))
+    for k in range(camg.nlevels):
+        if camg.levels[k].a.nrows >= 10000:
+            rows.append((f"coarse AMG A_{k}", camg.levels[k].a))
+    famg = h.amg(0)
+    for k in range(famg.nlevels):
+        if famg.levels[k].a.nrows >= 10000:
+            rows.append((f"F-relax AMG A_{k}", famg.levels[k].a))
     for name, m in rows:
         ms, byt = time_spmv(ctx, m, reps)
         print(f"{name:22s} rows={m.nrows:9d} nnz={m.nnz:10d} nnz/row={m.nnz/max(m.nrows,1)*(m.block_size**2)/m.block_size:6.1f} "
