@@ -437,6 +437,13 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       trace("mgr: R*(AP)");
       lv.Aff = extract(cur, lv.flist.p, lv.nf, fmap.p, lv.nf);
       trace("mgr: extract A_ff");
+      if (!post_smoothing && !sp.global_relax) {
+        // after the F-relaxation from e = 0, e is zero on C: r - A e = r - A[:, F] e_F
+        DBuf<int> allrows(n);
+        iota_i32(allrows.p, n);
+        lv.AF = extract(cur, allrows.p, n, fmap.p, lv.nf);
+        prepare_spmv(lv.AF);
+      }
       if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
       if (need_cells) {
         std::vector<int64_t> nxt_cells(lv.nc);
@@ -501,6 +508,7 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
   }
   MgrLevel &lv = h.L[k];
   bool zero = true;
+  bool f_only = false;  // e = [e_F; 0] exactly (F-relaxation from zero)
   if (lv.bd) {
     k_bd_apply<<<grid_for(lv.bd->nblk, 128), 128, 0, stream()>>>(lv.bd->nblk, lv.bd->ioff.p, lv.bd->moff.p,
                                                                  lv.bd->idx.p, lv.bd->inv.p, r, e);
@@ -509,7 +517,8 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
   }
   auto resid = [&]() -> const double * {
     if (zero) return r;
-    residual(lv.A, e, r, lv.res.p);
+    if (f_only && lv.AF.nr) residual(lv.AF, lv.eF.p, r, lv.res.p);  // skips the zero C columns
+    else residual(lv.A, e, r, lv.res.p);
     return lv.res.p;
   };
   auto f_relax = [&]() {
@@ -523,8 +532,13 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
       fsolve(lv.fs, lv.Aff, lv.rF.p, lv.eF.p);
     }
     ProfScope ps(4);
-    if (zero) fc_merge(e, lv.eF.p, lv.fmap.p, lv.n);  // e = [e_F; 0] in one pass
-    else scatter_add(e, lv.eF.p, lv.flist.p, lv.nf);
+    if (zero) {
+      fc_merge(e, lv.eF.p, lv.fmap.p, lv.n);  // e = [e_F; 0] in one pass
+      f_only = true;
+    } else {
+      scatter_add(e, lv.eF.p, lv.flist.p, lv.nf);
+      f_only = false;
+    }
     zero = false;
   };
   auto coarse_correct = [&]() {
@@ -538,6 +552,7 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
     if (zero) spmv(lv.P, lv.ec.p, e);
     else spmv_add(lv.P, lv.ec.p, e);
     zero = false;
+    f_only = false;
   };
   if (h.post_smoothing) {
     coarse_correct();

@@ -69,6 +69,7 @@ struct BlockDiag {             // per-cell block-diagonal relaxation (mgr.py:212
 
 struct MgrLevel {
   Csr A, R, P, Aff;
+  Csr AF;                      // A[:, F] (F-local columns): residual after F-relaxation from e = 0
   int n = 0, nf = 0, nc = 0, rp = 0;
   DBuf<int> flist, clist, fmap;
   FSolver fs;

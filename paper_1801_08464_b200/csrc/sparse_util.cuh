@@ -10,5 +10,7 @@ Csr transpose(const Csr &a);
 // rows_dev: nr source rows (sorted); cmap_dev: column map (source col -> new col or -1)
 Csr extract(const Csr &a, const int *rows_dev, int nr, const int *cmap_dev, int nc);
 Csr copy_csr(const Csr &a);
+// p[i] = i
+void iota_i32(int *p, int64_t n);
 void scale_i64(int64_t *a, int64_t s, int n);
 }  // namespace mg

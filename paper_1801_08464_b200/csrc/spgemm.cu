@@ -591,6 +591,12 @@ Csr extract(const Csr &a, const int *rows_dev, int nr, const int *cmap_dev, int 
   return o;
 }
 
+void iota_i32(int *p, int64_t n) {
+  if (n <= 0) return;
+  k_iota<<<grid_for(n, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(p, n);
+  check_launch("iota");
+}
+
 Csr copy_csr(const Csr &a) {
   Csr o;
   o.alloc(a.nr, a.nc, a.nnz, a.b);
