@@ -40,8 +40,6 @@ __device__ __forceinline__ int hash_insert_slot(int *keys, unsigned mask, int k,
 
 // Walk the products of A row `row` (j ascending, B_j stored order) in windows
 // of 32; calls f(valid, k, prod) with all lanes converged, in product order.
-// The global loads of window w+1 (column and value of B) are issued before
-// window w is processed, so their latency overlaps the hashing of window w.
 template <bool NEED_VAL, class F>
 __device__ __forceinline__ void for_products(int row, int lane, const int *__restrict__ arp,
                                              const int *__restrict__ aci, const double *__restrict__ av,
@@ -64,10 +62,10 @@ __device__ __forceinline__ void for_products(int row, int lane, const int *__res
       int y = __shfl_up_sync(0xffffffffu, incl, off);
       if (lane >= off) incl += y;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    // window loader: product p = w0 + lane -> (k, b value, a value)
-    auto load = [&](int w0, int &k, double &bval, double &aval) {
+    int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int w0 = 0; w0 < total; w0 += 32) {
       int p = w0 + lane;
+      // src = first lane with incl > p
       int lo = 0, hi = 31;
 #pragma unroll
       for (int it = 0; it < 5; ++it) {
@@ -75,31 +73,20 @@ __device__ __forceinline__ void for_products(int row, int lane, const int *__res
         int v = __shfl_sync(0xffffffffu, incl, mid);
         if (p < v) hi = mid; else lo = mid + 1;
       }
-      const int src = lo;
-      const int s_incl = __shfl_sync(0xffffffffu, incl, src);
-      const int s_len = __shfl_sync(0xffffffffu, len, src);
-      const int s_rb = __shfl_sync(0xffffffffu, rb, src);
-      aval = NEED_VAL ? __shfl_sync(0xffffffffu, a, src) : 0.0;
-      k = -1;
-      bval = 0.0;
-      if (p < total) {
+      int src = lo;
+      int s_incl = __shfl_sync(0xffffffffu, incl, src);
+      int s_len = __shfl_sync(0xffffffffu, len, src);
+      int s_rb = __shfl_sync(0xffffffffu, rb, src);
+      double s_a = NEED_VAL ? __shfl_sync(0xffffffffu, a, src) : 0.0;
+      bool valid = p < total;
+      int k = -1;
+      double prod = 0.0;
+      if (valid) {
         int r = s_rb + (p - (s_incl - s_len));
         k = __ldg(bci + r);
-        if (NEED_VAL) bval = __ldg(bv + r);
+        if (NEED_VAL) prod = __dmul_rn(s_a, __ldg(bv + r));
       }
-    };
-    int k0;
-    double b0, a0;
-    load(0, k0, b0, a0);
-    for (int w0 = 0; w0 < total; w0 += 32) {
-      int k1 = -1;
-      double b1 = 0.0, a1 = 0.0;
-      if (w0 + 32 < total) load(w0 + 32, k1, b1, a1);  // warp-uniform
-      const bool valid = w0 + lane < total;
-      f(valid, k0, NEED_VAL && valid ? __dmul_rn(a0, b0) : 0.0);
-      k0 = k1;
-      b0 = b1;
-      a0 = a1;
+      f(valid, k, prod);
     }
   }
 }
