@@ -122,7 +122,14 @@ static bool concurrent_setup() {
 
 void TaskGroup::run(std::function<void()> fn) {
   if (!concurrent_setup() || trace_on()) {
-    fn();
+    // inline: same error semantics as a worker (recorded, reported at the join)
+    std::exception_ptr e = nullptr;
+    try {
+      fn();
+    } catch (...) {
+      e = std::current_exception();
+    }
+    err_.push_back(e);
     return;
   }
   Ctx *p = parent_;
@@ -170,6 +177,12 @@ void TaskGroup::run(std::function<void()> fn) {
 }
 
 void TaskGroup::join() {
+  std::vector<std::exception_ptr> errs = join_errors();
+  for (auto &e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+std::vector<std::exception_ptr> TaskGroup::join_errors() {
   for (auto &t : th_)
     if (t.joinable()) t.join();
   th_.clear();
@@ -186,11 +199,9 @@ void TaskGroup::join() {
     neutralise_all(p);
   }
   used_.clear();
-  std::exception_ptr first = nullptr;
-  for (auto &e : err_)
-    if (e && !first) first = e;
-  err_.clear();
-  if (first) std::rethrow_exception(first);
+  std::vector<std::exception_ptr> errs;
+  errs.swap(err_);
+  return errs;
 }
 
 void sync() {

@@ -88,6 +88,8 @@ class TaskGroup {
   ~TaskGroup();
   void run(std::function<void()> fn);
   void join();
+  // join without throwing; the error of each task (nullptr if none), in run order
+  std::vector<std::exception_ptr> join_errors();
  private:
   Ctx *parent_;
   std::vector<std::thread> th_;

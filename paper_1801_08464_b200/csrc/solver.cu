@@ -404,6 +404,7 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
   h->coarse_kind = coarse_kind;
   h->L.reserve(plan.size());
   TaskGroup tasks;  // declared after h: joined before h can be destroyed
+  int parent_level = -1;  // MGR level this thread is building (task k = level k)
   try {
     Csr cur = copy_csr(a);
     // per-unknown owning cell, tracked down the levels only when a level relaxes globally
@@ -420,7 +421,9 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       int nf_h = 0;
       for (uint8_t m : sp.fmask) nf_h += m != 0;
       if (nf_h == 0 || nf_h == n) continue;
-      MgrLevel lv;
+      h->L.emplace_back();
+      MgrLevel &lv = h->L.back();  // stable: capacity reserved
+      parent_level = (int)h->L.size() - 1;
       lv.n = n;
       lv.rp = sp.rp;
       DBuf<uint8_t> mask(n);
@@ -429,14 +432,26 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       DBuf<int> &fmap = lv.fmap;
       fc_split(mask.p, n, lv.flist, lv.clist, fmap, cmap, lv.nf, lv.nc);
       trace("mgr: fc_split");
+      lv.Aff = extract(cur, lv.flist.p, lv.nf, fmap.p, lv.nf);
+      trace("mgr: extract A_ff");
+      // The F-relaxation setup (an AMG hierarchy on A_ff for FRelax('amg')) needs
+      // only A_ff: it runs on a worker stream while this thread builds R, P, the
+      // Galerkin product and everything below this level.
+      {
+        MgrLevel *lvp = &lv;
+        const LevelSpec *spp = &sp;
+        tasks.run([lvp, spp, ao]() {
+          fsolver_setup(lvp->fs, lvp->Aff, *spp, ao);
+          prepare_spmv(lvp->Aff);
+          trace("mgr: F-solver setup");
+        });
+      }
       build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
       trace("mgr: build_rp");
       Csr ap = spgemm(cur, lv.P);
       trace("mgr: A*P");
       Csr ac = spgemm(lv.R, ap);
       trace("mgr: R*(AP)");
-      lv.Aff = extract(cur, lv.flist.p, lv.nf, fmap.p, lv.nf);
-      trace("mgr: extract A_ff");
       if (!post_smoothing && !sp.global_relax) {
         // after the F-relaxation from e = 0, e is zero on C: r - A e = r - A[:, F] e_F
         DBuf<int> allrows(n);
@@ -462,18 +477,8 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       lv.ec.alloc(lv.nc);
       lv.A = std::move(cur);
       cur = std::move(ac);
-      h->L.push_back(std::move(lv));
-      // The F-relaxation setup (an AMG hierarchy on A_ff for FRelax('amg')) is
-      // independent of everything below this level: it runs concurrently on a
-      // worker stream while this thread builds the next level / coarse AMG.
-      MgrLevel *lvp = &h->L.back();  // stable: capacity reserved
-      const LevelSpec *spp = &sp;
-      tasks.run([lvp, spp, ao]() {
-        fsolver_setup(lvp->fs, lvp->Aff, *spp, ao);
-        prepare_spmv(lvp->Aff);
-        trace("mgr: F-solver setup");
-      });
     }
+    parent_level = 1 << 30;  // below every level
     trace("mgr: levels done");
     if (coarse_kind == 0) {
       h->camg = amg_setup(cur, ao);
@@ -490,13 +495,16 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
     }
     h->coarse_A = std::move(cur);
   } catch (...) {
-    // a failing F-relaxation setup of an earlier level takes precedence (the
-    // reference reports errors in level order)
+    // errors in the reference's order (mgr.py:280-300): per level build_rp,
+    // RAP, then the F-solver; a failing F-solver of an earlier level wins over
+    // this thread's error, this level's F-solver error loses to it
     std::exception_ptr pe = std::current_exception();
-    tasks.join();
+    std::vector<std::exception_ptr> we = tasks.join_errors();
+    for (int k = 0; k < (int)we.size() && k < parent_level; ++k)
+      if (we[k]) std::rethrow_exception(we[k]);
     std::rethrow_exception(pe);
   }
-  tasks.join();
+  tasks.join();  // F-solver errors of any level
   return h;
 }
 
