@@ -58,6 +58,7 @@ class ClockSampler:
         self.device = device
         self.rows = []
         self.proc = None
+        self.i0 = 0
 
     def start(self):
         try:
@@ -73,20 +74,27 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
+    def mark(self):
+        """Start of the timed region: only samples from here on are summarised.
+        (nvidia-smi is started before the warm-up so that its start-up, which
+        briefly stalls the driver, is not inside the timed region.)"""
+        self.i0 = len(self.rows)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = list(self.rows[self.i0:]) or list(self.rows)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:  # noqa: BLE001
             self.proc.kill()
         self.t.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             if len(r) < 7:
                 continue
             for k, nm in enumerate(names):
@@ -212,12 +220,13 @@ def main():
         ctx.sync()
         rep.barrier()
 
+    clk = ClockSampler(local)
+    clk.start()  # before the warm-up: nvidia-smi's start-up stalls the driver briefly
     for _ in range(args.warmup):
         device_step()
     barrier()
     # ---- timed region (device-resident inputs) --------------------------------------
-    clk = ClockSampler(local)
-    clk.start()
+    clk.mark()
     launches0 = ctx.launches
     its = []
     conv = True

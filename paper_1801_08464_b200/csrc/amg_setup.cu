@@ -134,10 +134,12 @@ __global__ void k_strength(int n, const int *rp, const int *ci, const double *v,
     double cand = (off && a < 0.0) ? -a : ((off && !has_neg) ? fabs(a) : 0.0);
     int8_t st = (rmax > 0.0 && cand >= thr) ? 1 : 0;
     s[q] = st;
-    cnt += st;
+    cnt |= st;
   }
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0 && cnt) atomicAdd(any, cnt);
+  // only "some strong edge exists" is consumed: one atomic the first time a
+  // warp sees an unset flag (a counter hit by every row serialised the kernel)
+  unsigned has = __ballot_sync(0xffffffffu, cnt != 0);
+  if (lane == 0 && has && *(volatile int *)any == 0) atomicExch(any, 1);
 }
 
 int64_t strength(const Csr &a, double theta, DBuf<int8_t> &s) {
@@ -183,7 +185,7 @@ __global__ void k_pmis_init(int n, const int *trp, uint64_t seed, int level, dou
   double u = __dmul_rn((double)(splitmix64(x) >> 11), 1.0 / 9007199254740992.0);
   mu[i] = __dadd_rn((double)st, u);
   state[i] = st == 0 ? FPT : UNDEC;
-  if (st) atomicAdd(undecided, 1);
+  if (st && *(volatile int *)undecided == 0) atomicExch(undecided, 1);  // only "any" is consumed
 }
 __device__ __forceinline__ bool beats(double mi, int i, double mj, int j) {
   return mi > mj || (mi == mj && i > j);
@@ -220,7 +222,9 @@ __global__ void k_pmis_update(int n, const int *rp, const int *ci, const int8_t 
     int k = ci[q];
     if (s[q] && k != i && (newc[k] || state[k] == CPT)) { state[i] = FPT; return; }
   }
-  atomicAdd(undecided, 1);
+  // termination only needs "some point is still undecided": set the flag once
+  // (a counter incremented by every undecided row serialised the early rounds)
+  if (*(volatile int *)undecided == 0) atomicExch(undecided, 1);
 }
 
 int pmis(const Csr &a, const int8_t *s, uint64_t seed, int level, DBuf<int8_t> &state) {

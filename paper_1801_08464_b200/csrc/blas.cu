@@ -304,6 +304,119 @@ __global__ void __launch_bounds__(RB) k_combine(const double *__restrict__ V, in
   }
 }
 
+// ---- one-reduction CGS2 with delayed reorthogonalisation (DCGS2) -------------------
+// Dot pass: out = [V^T u, V^T w] for the K = j+1 stored vectors (V[j] = u, the
+// provisional new basis vector) against u and the new Krylov vector w, reading
+// V once: each warp owns vectors k, k + nw, ... over a chunk of MCH elements
+// (u and w shared through L1); blocks of nw = min(K, 8) warps keep every warp
+// busy for small K.
+__global__ void __launch_bounds__(256) k_mdot2x(const double *__restrict__ V, int64_t ldv, int K,
+                                               const double *__restrict__ u, const double *__restrict__ w,
+                                               int64_t n, double *partial) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double au[4] = {0.0, 0.0, 0.0, 0.0}, aw[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t c0 = (int64_t)blockIdx.x * MCH; c0 < n; c0 += (int64_t)gridDim.x * MCH) {
+    int64_t cend = c0 + MCH < n ? c0 + MCH : n;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int k = wid + nw * q;
+      if (k >= K) break;
+      const double *vk = V + k * ldv;
+      double a = 0.0, b = 0.0;
+      int64_t i = c0 + lane;
+      for (; i + 32 < cend; i += 64) {
+        double v0 = __ldcs(vk + i), v1 = __ldcs(vk + i + 32);
+        double u0 = __ldg(u + i), u1 = __ldg(u + i + 32);
+        double w0 = __ldg(w + i), w1 = __ldg(w + i + 32);
+        a += v0 * u0 + v1 * u1;
+        b += v0 * w0 + v1 * w1;
+      }
+      for (; i < cend; i += 32) {
+        double v0 = __ldcs(vk + i);
+        a += v0 * __ldg(u + i);
+        b += v0 * __ldg(w + i);
+      }
+      au[q] += a;
+      aw[q] += b;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double a = au[q], b = aw[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, off);
+      b += __shfl_down_sync(0xffffffffu, b, off);
+    }
+    int k = wid + nw * q;
+    if (lane == 0 && k < K) {
+      partial[(int64_t)blockIdx.x * 2 * K + k] = a;
+      partial[(int64_t)blockIdx.x * 2 * K + K + k] = b;
+    }
+  }
+}
+
+// Update pass, one read of the j finalised vectors Q = V[0..j):
+//   q_j     = (sigma u - Q s) / alpha             -> V[j]   (u read from V[j])
+//   u_{j+1} = (sigma w - Q e - gamma sigma u) / alpha -> V[j+1]; partial ||u_{j+1}||^2
+// coef = [s (j), e (j), sigma, 1/alpha, gamma]
+__global__ void __launch_bounds__(RB) k_dcgs2_update(double *V, int64_t ldv, int j,
+                                                    const double *__restrict__ coef,
+                                                    const double *__restrict__ w, int64_t n,
+                                                    double *partial) {
+  __shared__ double cs[32], ce[32], sc[3];
+  if (threadIdx.x < 32) {
+    cs[threadIdx.x] = (int)threadIdx.x < j ? coef[threadIdx.x] : 0.0;
+    ce[threadIdx.x] = (int)threadIdx.x < j ? coef[j + threadIdx.x] : 0.0;
+  }
+  if (threadIdx.x < 3) sc[threadIdx.x] = coef[2 * j + threadIdx.x];
+  __syncthreads();
+  const double sigma = sc[0], inva = sc[1], gamma = sc[2];
+  double *uj = V + (int64_t)j * ldv, *un = V + (int64_t)(j + 1) * ldv;
+  double acc[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+    double a = 0.0, b = 0.0;
+    for (int k0 = 0; k0 < j; k0 += 8) {
+      double vk[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) vk[t] = k0 + t < j ? __ldcs(V + (k0 + t) * ldv + i) : 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        a += cs[(k0 + t) & 31] * vk[t];
+        b += ce[(k0 + t) & 31] * vk[t];
+      }
+    }
+    const double u = sigma * uj[i];
+    const double nu = (sigma * __ldg(w + i) - b - gamma * u) * inva;
+    uj[i] = (u - a) * inva;
+    un[i] = nu;
+    acc[0] += nu * nu;
+  }
+  block_reduce_store<1>(acc, 1, partial);
+}
+
+void mdot2x(const double *V, int64_t ldv, int K, const double *u, const double *w, int64_t n, double *out_dev) {
+  if (K > 32) throw MgError(MG_ERR_UNSUPPORTED, "mdot2x: at most 32 vectors");
+  const int nw = K < 8 ? K : 8;
+  int64_t want = (n + MCH - 1) / MCH;
+  int64_t cap = (int64_t)g_ctx->num_sms * 8 * (8 / nw);
+  int nb = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  double *part = red_scratch((size_t)nb * 64);
+  k_mdot2x<<<nb, 32 * nw, 0, stream()>>>(V, ldv, K, u, w, n, part);
+  check_launch("mdot2x");
+  reduce_finish(part, nb, 2 * K, out_dev);
+}
+
+void dcgs2_update(double *V, int64_t ldv, int j, const double *coef_dev, const double *w, int64_t n,
+                  double *norm2_dev) {
+  if (j > 32) throw MgError(MG_ERR_UNSUPPORTED, "dcgs2_update: at most 32 vectors");
+  int nb = red_blocks(n);
+  double *part = red_scratch((size_t)nb + 8);
+  k_dcgs2_update<<<nb, RB, 0, stream()>>>(V, ldv, j, coef_dev, w, n, part);
+  check_launch("dcgs2_update");
+  reduce_finish(part, nb, 1, norm2_dev);
+}
+
 #define KSEL(K, CALL16, CALL32) \
   do { if ((K) <= 16) { CALL16; } else { CALL32; } } while (0)
 

@@ -40,6 +40,13 @@ void update_mdot(const double *V, int64_t ldv, int K, const double *c_dev, doubl
 // w -= sum_k c[k] V_k ; out[0] = ||w||^2
 void update_norm2(const double *V, int64_t ldv, int K, const double *c_dev, double *w, int64_t n,
                   double *out_dev);
+// DCGS2 (one reduction per Arnoldi step, delayed reorthogonalisation):
+// out = [V^T u (K), V^T w (K)], K <= 32
+void mdot2x(const double *V, int64_t ldv, int K, const double *u, const double *w, int64_t n, double *out_dev);
+// V[j] = (sigma V[j] - Q s)/alpha; V[j+1] = (sigma w - Q e - gamma sigma V[j])/alpha; norm2 = ||V[j+1]||^2
+// coef = [s (j), e (j), sigma, 1/alpha, gamma], j <= 32
+void dcgs2_update(double *V, int64_t ldv, int j, const double *coef_dev, const double *w, int64_t n,
+                  double *norm2_dev);
 // u = sum_k y[k] V_k
 void combine(const double *V, int64_t ldv, int K, const double *y_dev, double *u, int64_t n);
 

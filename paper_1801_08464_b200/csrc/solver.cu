@@ -678,9 +678,17 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
     return use_anorm && res <= o.rel_tol * (a_norm * xn + b_norm);
   };
   int mmax = std::min(o.restart, o.max_iter);
+  // DCGS2 (default with reorthogonalisation, restart <= 31); MG_GMRES_CGS2=1 keeps classic CGS2
+  static int classic = -1;
+  if (classic < 0) {
+    const char *e = getenv("MG_GMRES_CGS2");
+    classic = e && *e == '1';
+  }
+  const bool dcgs2 = o.reorth && !classic && mmax <= 31;
   // basis row stride padded off a power of two (K streams 32 MB apart otherwise collide)
   const int64_t ldv = ((n + 1) & ~(int64_t)1) + 1024;
-  DBuf<double> V((size_t)(mmax + 1) * ldv), w(n), z(n), r(n), xt(n), u(n), t(n), proj((size_t)2 * (mmax + 1) + 8);
+  DBuf<double> V((size_t)(mmax + 1) * ldv), w(n), z(n), r(n), xt(n), u(n), t(n), proj((size_t)2 * (mmax + 1) + 8),
+      coefd(2 * 32 + 3);
   double *c_dev = proj.p, *c2_dev = proj.p + (mmax + 1), *nrm_dev = proj.p + 2 * (mmax + 1);
   std::vector<double> hbuf(2 * (mmax + 1) + 1);
   vfill(x, 0.0, n);
@@ -738,6 +746,122 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
     int k = 0;
     bool early = false;
     double early_res = 0.0;
+    if (dcgs2) {
+      // One-reduction CGS2 with delayed reorthogonalisation (DCGS2): V[j] holds
+      // the once-orthogonalised u_j (unnormalised); one dot pass gives
+      // [Q^T u, Q^T w, u.u, u.w], the update pass finalises q_j (the second
+      // CGS pass of u_j) and forms u_{j+1} from w in the same read of Q.  The
+      // provisional column j-1 of H is corrected with the reorthogonalisation
+      // coefficients (h += beta s, h_{j,j-1} = beta alpha), and the first
+      // projection of w is reconstructed from Q^T w through the Arnoldi
+      // relation of the corrected columns.  Two basis passes per step instead
+      // of CGS2's four; GMRES's decisions use the same Givens / |g| tests.
+      std::vector<double> Hr((size_t)(mm + 1) * mm, 0.0), coef(2 * 32 + 3), sv(mm), tv(mm), cvec(mm + 1);
+      auto hr = [&](int i, int jj) -> double & { return Hr[(size_t)i * mm + jj]; };
+      auto givens = [&](int kc) {  // H, g <- QR of the first kc raw columns
+        for (size_t q = 0; q < H.size(); ++q) H[q] = Hr[q];
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = res;
+        for (int jj = 0; jj < kc; ++jj) {
+          for (int i = 0; i < jj; ++i) {
+            double t0 = cs[i] * h_at(i, jj) + sn[i] * h_at(i + 1, jj);
+            h_at(i + 1, jj) = -sn[i] * h_at(i, jj) + cs[i] * h_at(i + 1, jj);
+            h_at(i, jj) = t0;
+          }
+          double den = std::hypot(h_at(jj, jj), h_at(jj + 1, jj));
+          if (den == 0.0) return jj;
+          cs[jj] = h_at(jj, jj) / den;
+          sn[jj] = h_at(jj + 1, jj) / den;
+          h_at(jj, jj) = den;
+          h_at(jj + 1, jj) = 0.0;
+          g[jj + 1] = -sn[jj] * g[jj];
+          g[jj] = cs[jj] * g[jj];
+        }
+        return kc;
+      };
+      for (int j = 0; j < mm; ++j) {
+        double *vj = V.p + (int64_t)j * ldv;
+        const double *mz = precond(vj, z.p);
+        op_apply(a, mz, w.p);
+        {
+          ProfScope ps(3);
+          mdot2x(V.p, ldv, j + 1, vj, w.p, n, proj.p);
+        }
+        {
+          ProfScope ps(6);
+          d2h(hbuf.data(), proj.p, sizeof(double) * (2 * (j + 1)));
+        }
+        const int K = j + 1;
+        const double uu_raw = hbuf[j], uw_raw = hbuf[K + j];
+        const double bt = std::sqrt(uu_raw), sigma = 1.0 / bt;
+        double ss = 0.0, st = 0.0;
+        for (int i = 0; i < j; ++i) {
+          sv[i] = sigma * hbuf[i];
+          tv[i] = sigma * hbuf[K + i];
+          ss += sv[i] * sv[i];
+          st += sv[i] * tv[i];
+        }
+        const double a2 = sigma * sigma * uu_raw - ss;
+        if (!(a2 > 0.0) || !(bt > 0.0)) {  // u_j in span(Q): breakdown
+          k = j;
+          break;
+        }
+        const double alpha = std::sqrt(a2);
+        if (j >= 1) {  // delayed correction of column j-1 (provisional h_{j,j-1} = bt)
+          for (int i = 0; i < j; ++i) hr(i, j - 1) += bt * sv[i];
+          hr(j, j - 1) = bt * alpha;
+        }
+        for (int i = 0; i <= j; ++i) {
+          double c = 0.0;
+          for (int q = 0; q < j; ++q) c += hr(i, q) * sv[q];
+          cvec[i] = c;
+        }
+        const double qw = (sigma * sigma * uw_raw - st) / alpha;
+        for (int i = 0; i < j; ++i) hr(i, j) = (tv[i] - cvec[i]) / alpha;
+        hr(j, j) = (qw - cvec[j]) / alpha;
+        const double gam = qw / alpha;
+        for (int i = 0; i < j; ++i) {
+          coef[i] = sv[i];
+          coef[j + i] = tv[i] - gam * sv[i];
+        }
+        coef[2 * j] = sigma;
+        coef[2 * j + 1] = 1.0 / alpha;
+        coef[2 * j + 2] = gam;
+        MG_CUDA(cudaMemcpyAsync(coefd.p, coef.data(), sizeof(double) * (2 * j + 3), cudaMemcpyHostToDevice,
+                                stream()));
+        {
+          ProfScope ps(3);
+          dcgs2_update(V.p, ldv, j, coefd.p, w.p, n, nrm_dev);
+        }
+        double nrm2v = 0.0;
+        {
+          ProfScope ps(6);
+          d2h(&nrm2v, nrm_dev, sizeof(double));
+        }
+        const double hn = std::sqrt(nrm2v);
+        hr(j + 1, j) = hn;  // provisional until the next step's reorthogonalisation
+        ++total;
+        k = j + 1;
+        int kq = givens(k);
+        if (kq < k) {
+          k = kq;
+          break;
+        }
+        bool happy = hn <= 1e-14 * std::max(res, 1.0);
+        if (std::fabs(g[j + 1]) <= tol || happy || total >= o.max_iter) break;
+        if (use_anorm && o.check_every && k % o.check_every == 0) {
+          assemble(k, xt.p);
+          op_apply(a, xt.p, t.p);
+          vsub(r.p, b, t.p, n);
+          double rt = nrm2(r.p, n);
+          if (accepted(rt, nrm2(xt.p, n))) {
+            early = true;
+            early_res = rt;
+            break;
+          }
+        }
+      }
+    } else
     for (int j = 0; j < mm; ++j) {
       double *vj = V.p + (int64_t)j * ldv;
       const double *mz = precond(vj, z.p);
