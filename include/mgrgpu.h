@@ -32,7 +32,8 @@ enum {
   MG_ERR_BAD_OPTION = 4,    /* ValueError (bad options / empty F or C sets) mgr.py:121  */
   MG_ERR_CUDA = 5,          /* CUDA runtime failure (no silent fallback)               */
   MG_ERR_SINGULAR = 6,      /* ncpflow.sparse.SingularMatrixError sparse.py:22-28      */
-  MG_ERR_UNSUPPORTED = 7    /* feature not available on the GPU path                    */
+  MG_ERR_UNSUPPORTED = 7,   /* feature not available on the GPU path                    */
+  MG_ERR_ZERO_PIVOT = 8     /* ncpflow.ilu.ZeroPivot(row)        ilu.py:24-27,131-140   */
 };
 
 typedef struct mg_ctx mg_ctx;
@@ -101,6 +102,19 @@ int mg_block_apply(mg_ctx *ctx, const mg_mat *dinv, const double *v, double *z);
 int mg_equilibrate(mg_ctx *ctx, const mg_mat *a, mg_mat **scaled_out, double *row_out, double *col_scale_out);
 /* max_i sum_j |a_ij| of a scalar CSR matrix (the a_norm of linsolve.py:97-98) */
 int mg_abs_row_sum_max(mg_ctx *ctx, const mg_mat *a, double *out);
+
+/* ---- ILU(k) comparator (ilu.py:53-174) ------------- */
+typedef struct mg_ilu mg_ilu;
+/* level-k incomplete LU of a square scalar CSR matrix (symbolic level-of-fill
+ * closure on the host for k >= 1, numeric IKJ elimination on the device, no
+ * pivoting).  MG_ERR_ZERO_PIVOT with the reference's row via
+ * mg_last_error_row. */
+int mg_ilu_factor(mg_ctx *ctx, const mg_mat *a, int level, mg_ilu **out);
+/* combined L\U factor (unit lower diagonal implicit), as IluFactorization.matrix */
+int mg_ilu_matrix(mg_ctx *ctx, const mg_ilu *f, mg_mat **out);
+/* x = U^-1 L^-1 r (host vectors) */
+int mg_ilu_apply(mg_ctx *ctx, mg_ilu *f, const double *r, double *x);
+int mg_ilu_free(mg_ctx *ctx, mg_ilu *f);
 
 /* ---- MGR build_rp (mgr.py:117-156) ------------------------------------------ */
 enum { MG_RP_INJECTIVE = 0, MG_RP_NONINJECTIVE = 1, MG_RP_INJECTION = 2, MG_RP_IDEAL = 3 };
@@ -185,6 +199,10 @@ int mg_gmres(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b, double *x
              const mg_gmres_opts *opts, double a_norm, mg_gmres_result *res);
 int mg_gmres_dev(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b_dev, double *x_dev,
                  const mg_gmres_opts *opts, double a_norm, mg_gmres_result *res);
+/* GMRES preconditioned by an ILU factorisation (GmresSolver(preconditioner='ilu'),
+ * linsolve.py:79-84); host vectors */
+int mg_gmres_ilu(mg_ctx *ctx, const mg_mat *a, mg_ilu *f, const double *b, double *x, const mg_gmres_opts *opts,
+                 double a_norm, mg_gmres_result *out);
 
 /* ---- device buffers (bench / e2e plumbing) --------------------------------- */
 int mg_dev_alloc(mg_ctx *ctx, int64_t bytes, void **out);

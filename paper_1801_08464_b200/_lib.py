@@ -88,6 +88,11 @@ _SIGS = {
     "mg_mgr_free": [P, P],
     "mg_gmres": [P, P, P, P, P, ctypes.POINTER(GmresOpts), c_double, ctypes.POINTER(GmresRes)],
     "mg_gmres_dev": [P, P, P, P, P, ctypes.POINTER(GmresOpts), c_double, ctypes.POINTER(GmresRes)],
+    "mg_gmres_ilu": [P, P, P, P, P, ctypes.POINTER(GmresOpts), c_double, ctypes.POINTER(GmresRes)],
+    "mg_ilu_factor": [P, P, c_int, ctypes.POINTER(P)],
+    "mg_ilu_matrix": [P, P, ctypes.POINTER(P)],
+    "mg_ilu_apply": [P, P, P, P],
+    "mg_ilu_free": [P, P],
     "mg_dev_alloc": [P, c_int64, ctypes.POINTER(P)],
     "mg_dev_free": [P, P],
     "mg_memcpy_h2d": [P, P, P, c_int64],

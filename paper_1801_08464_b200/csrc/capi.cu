@@ -18,6 +18,7 @@ struct mg_amg {
   ~mg_amg() { if (owned) delete h; }
 };
 struct mg_mgr { std::unique_ptr<Mgr> h; };
+struct mg_ilu { std::unique_ptr<Ilu> f; };
 
 namespace {
 struct Enter {
@@ -473,7 +474,7 @@ int mg_mgr_free(mg_ctx *ctx, mg_mgr *h) {
 }
 
 static int gmres_common(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b_dev, double *x_dev,
-                        const mg_gmres_opts *opts, double a_norm, mg_gmres_result *res) {
+                        const mg_gmres_opts *opts, double a_norm, mg_gmres_result *res, Ilu *ilu = nullptr) {
   GmresOpts o;
   if (opts) {
     o.rel_tol = opts->rel_tol;
@@ -487,7 +488,7 @@ static int gmres_common(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b
   cudaEventCreate(&e1);
   prof_reset();
   cudaEventRecord(e0, stream());
-  GmresOut out = gmres(a->m, m ? m->h.get() : nullptr, b_dev, x_dev, o, a_norm);
+  GmresOut out = gmres(a->m, m ? m->h.get() : nullptr, b_dev, x_dev, o, a_norm, ilu);
   cudaEventRecord(e1, stream());
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -519,6 +520,45 @@ int mg_gmres(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b, double *x
 int mg_gmres_dev(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b_dev, double *x_dev,
                  const mg_gmres_opts *opts, double a_norm, mg_gmres_result *res) {
   return guard(ctx, [&] { gmres_common(ctx, a, m, b_dev, x_dev, opts, a_norm, res); });
+}
+
+int mg_gmres_ilu(mg_ctx *ctx, const mg_mat *a, mg_ilu *f, const double *b, double *x, const mg_gmres_opts *opts,
+                 double a_norm, mg_gmres_result *out) {
+  return guard(ctx, [&] {
+    int64_t n = vec_len(a->m);
+    DevVec db(b, n), dx(nullptr, n);
+    gmres_common(ctx, a, nullptr, db.b.p, dx.b.p, opts, a_norm, out, f ? f->f.get() : nullptr);
+    d2h(x, dx.b.p, sizeof(double) * n);
+  });
+}
+
+int mg_ilu_factor(mg_ctx *ctx, const mg_mat *a, int level, mg_ilu **out) {
+  return guard(ctx, [&] {
+    auto h = std::make_unique<mg_ilu>();
+    h->f = ilu_factor(a->m, level);
+    *out = h.release();
+  });
+}
+
+int mg_ilu_matrix(mg_ctx *ctx, const mg_ilu *f, mg_mat **out) {
+  return guard(ctx, [&] {
+    auto m = std::make_unique<mg_mat>();
+    m->m = copy_csr(f->f->LU);
+    *out = m.release();
+  });
+}
+
+int mg_ilu_apply(mg_ctx *ctx, mg_ilu *f, const double *r, double *x) {
+  return guard(ctx, [&] {
+    int64_t n = f->f->n;
+    DevVec dr(r, n), dx(nullptr, n);
+    ilu_apply(*f->f, dr.b.p, dx.b.p);
+    d2h(x, dx.b.p, sizeof(double) * n);
+  });
+}
+
+int mg_ilu_free(mg_ctx *ctx, mg_ilu *f) {
+  return guard(ctx, [&] { delete f; });
 }
 
 int mg_dev_alloc(mg_ctx *ctx, int64_t bytes, void **out) {

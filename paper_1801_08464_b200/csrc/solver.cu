@@ -38,12 +38,23 @@ void prof_reset() {
   g_ctx->timing.k0_ms = 0.0;
   g_ctx->timing.k0_calls = 0;
 }
+static bool level_prof() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_PROF_LEVELS");
+    on = e && *e == '1';
+  }
+  return on;
+}
+
 void prof_collect() {
   if (g_prof.empty()) return;
   cudaStreamSynchronize(stream());
+  double lev[100] = {0};
   for (auto &r : g_prof) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
+    if (r.kind >= 100 && r.kind < 200) lev[r.kind - 100] += ms;
     if (r.kind >= 0 && r.kind < 8) g_ctx->timing.phase_ms[r.kind] += ms;
     if (r.kind == 8) { g_ctx->timing.k0_ms += ms; g_ctx->timing.k0_calls++; }
     if (r.kind == 0) { g_ctx->timing.spmv_ms += ms; g_ctx->timing.spmv_calls++; }
@@ -52,6 +63,12 @@ void prof_collect() {
     cudaEventDestroy(r.b);
   }
   g_prof.clear();
+  if (level_prof()) {  // diagnostics: inclusive / exclusive V-cycle time per AMG level
+    for (int hh = 0; hh < 2; ++hh)
+      for (int l = 0; l < 50 && lev[hh * 50 + l] > 0; ++l)
+        fprintf(stderr, "[mg] %s AMG level %d: inclusive %.3f ms, exclusive %.3f ms\n", hh ? "F-relax" : "coarse",
+                l, lev[hh * 50 + l], lev[hh * 50 + l] - (l + 1 < 50 ? lev[hh * 50 + l + 1] : 0.0));
+  }
 }
 
 // ================================ AMG ==============================================
@@ -159,6 +176,7 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
 }
 
 static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero) {
+  ProfScope plev(level_prof() && l < 50 ? 100 + (h.tag_k0 ? 0 : 50) + l : -1);
   AmgLevel &v = h.L[l];
   if (l + 1 == (int)h.L.size()) {
     dense_matvec(h.cinv.p, b, x, h.cn);
@@ -657,7 +675,7 @@ static void op_apply(const Csr &a, const double *x, double *y) {
   spmv(a, x, y);
 }
 
-GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts &o, double a_norm) {
+GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts &o, double a_norm, Ilu *ilu) {
   int64_t n = (int64_t)a.nr * a.b;
   if ((int64_t)a.nc * a.b != n) throw MgError(MG_ERR_DIM_MISMATCH, "gmres: square operator required");
   if (m && m->n0 != n) throw MgError(MG_ERR_DIM_MISMATCH, "gmres: preconditioner dimension mismatch");
@@ -693,7 +711,12 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
   std::vector<double> hbuf(2 * (mmax + 1) + 1);
   vfill(x, 0.0, n);
   int total = 0;
+  if (ilu && ilu->n != n) throw MgError(MG_ERR_DIM_MISMATCH, "gmres: preconditioner dimension mismatch");
   auto precond = [&](const double *v, double *out_) -> const double * {
+    if (ilu) {
+      ilu_apply(*ilu, v, out_);
+      return out_;
+    }
     if (!m) return v;
     mgr_apply(*m, v, out_);
     return out_;

@@ -102,6 +102,17 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
                                int coarse_kind, bool post_smoothing, const int64_t *cells_host);
 void mgr_apply(Mgr &h, const double *r, double *e);
 
+// ILU(k) comparator (ilu.cu; ilu.py:53-174)
+struct Ilu {
+  Csr LU;                      // combined factor, sorted columns, unit lower diagonal implicit
+  DBuf<int> dpos;              // diagonal position per row
+  DBuf<int> ctrl;              // substitution ticket + ready flags
+  DBuf<double> t;              // intermediate of the two substitutions
+  int n = 0, level = 0;
+};
+std::unique_ptr<Ilu> ilu_factor(const Csr &a, int level);
+void ilu_apply(Ilu &f, const double *r, double *x);
+
 struct GmresOpts {
   double rel_tol = 1e-12;
   int max_iter = 400, restart = 30, reorth = 1, check_every = 25;
@@ -110,7 +121,8 @@ struct GmresOut {
   int iterations = 0, converged = 0;
   double residual_norm = 0, rhs_norm = 0;
 };
-GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts &o, double a_norm);
+GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts &o, double a_norm,
+               Ilu *ilu = nullptr);
 
 // build_rp (mgr_ops.cu)
 void fc_split(const uint8_t *fmask_dev, int n, DBuf<int> &flist, DBuf<int> &clist, DBuf<int> &fmap,

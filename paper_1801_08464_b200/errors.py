@@ -8,13 +8,13 @@ switch; otherwise they are standalone with the same names and bases
 from __future__ import annotations
 
 try:  # pragma: no cover - only where the reference is installed
-    from ncpflow import amg as _ramg, mgr as _rmgr, newton as _rnewton, sparse as _rsparse
+    from ncpflow import amg as _ramg, ilu as _rilu, mgr as _rmgr, newton as _rnewton, sparse as _rsparse
     _BASES = dict(zero=(_rmgr.ZeroFDiagonal,), amg=(_ramg.AmgSetupError,),
                   dim=(_rsparse.DimensionMismatch,), sing=(_rsparse.SingularMatrixError,),
-                  lsf=(_rnewton.LinearSolveFailure,))
+                  lsf=(_rnewton.LinearSolveFailure,), piv=(_rilu.ZeroPivot,))
 except Exception:  # noqa: BLE001
     _BASES = dict(zero=(RuntimeError,), amg=(RuntimeError,), dim=(ValueError,), sing=(RuntimeError,),
-                  lsf=(RuntimeError,))
+                  lsf=(RuntimeError,), piv=(RuntimeError,))
 
 
 class ZeroFDiagonal(*_BASES["zero"]):
@@ -42,6 +42,14 @@ class LinearSolveFailure(*_BASES["lsf"]):
     pass
 
 
+class ZeroPivot(*_BASES["piv"]):
+    """ILU zero pivot (ilu.py:24-27)."""
+
+    def __init__(self, row):
+        RuntimeError.__init__(self, f"zero pivot encountered at row {row}")
+        self.row = row
+
+
 class UnsupportedOnGpu(NotImplementedError):
     pass
 
@@ -63,4 +71,6 @@ def from_status(st: int, msg: str, row: int):
         return SingularMatrixError(row, 0.0, msg)
     if st == 7:
         return UnsupportedOnGpu(msg)
+    if st == 8:
+        return ZeroPivot(row)
     return CudaError(f"libmgrgpu CUDA failure: {msg}")

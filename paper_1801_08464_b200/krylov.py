@@ -59,10 +59,11 @@ def _as_operator(apply_a) -> DeviceMatrix:
 
 
 def _as_precond(apply_m):
-    if apply_m is None or isinstance(apply_m, MgrHierarchy):
+    from .ilu import IluFactorization
+    if apply_m is None or isinstance(apply_m, (MgrHierarchy, IluFactorization)):
         return apply_m
-    raise TypeError("gmres on the GPU needs apply_m to be an MgrHierarchy (or None); a Python callable "
-                    "cannot run on the device")
+    raise TypeError("gmres on the GPU needs apply_m to be an MgrHierarchy or IluFactorization (or None); a "
+                    "Python callable cannot run on the device")
 
 
 def gmres(apply_a, apply_m, b, opts: GmresOptions = GmresOptions(), a_norm: float | None = None) -> GmresResult:
@@ -76,7 +77,12 @@ def gmres(apply_a, apply_m, b, opts: GmresOptions = GmresOptions(), a_norm: floa
     x = np.empty_like(b)
     res = _lib.GmresRes()
     c = opts.to_c()
-    a.ctx.call("mg_gmres", a.h, None if m is None else m.h, _lib.ptr(b), _lib.ptr(x), ctypes.byref(c),
-               -1.0 if a_norm is None else float(a_norm), ctypes.byref(res))
+    from .ilu import IluFactorization
+    if isinstance(m, IluFactorization):
+        a.ctx.call("mg_gmres_ilu", a.h, m.h, _lib.ptr(b), _lib.ptr(x), ctypes.byref(c),
+                   -1.0 if a_norm is None else float(a_norm), ctypes.byref(res))
+    else:
+        a.ctx.call("mg_gmres", a.h, None if m is None else m.h, _lib.ptr(b), _lib.ptr(x), ctypes.byref(c),
+                   -1.0 if a_norm is None else float(a_norm), ctypes.byref(res))
     return GmresResult(x, int(res.iterations), bool(res.converged), float(res.residual_norm),
                        float(res.rhs_norm))

@@ -15,8 +15,9 @@ mgr_specs, amg_opts, ilu_level, post_smoothing, equilibrate) and
   * ``a_norm`` = max row abs sum of the (scaled) matrix (linsolve.py:97-98)
     and right-preconditioned GMRES with the backward-error acceptance.
 
-Not on the GPU: preconditioner='ilu' (the ILU(k) comparator, SURVEY.md §8(f)
-item 4) raises ``UnsupportedOnGpu``.
+preconditioner='ilu' builds the ILU(ilu_level) comparator on the device
+(``ilu.ilu_factor``; a zero pivot becomes ``LinearSolveFailure`` as in
+linsolve.py:79-83).
 """
 from __future__ import annotations
 
@@ -26,7 +27,8 @@ import numpy as np
 
 from . import _lib
 from .amg import AmgOptions
-from .errors import LinearSolveFailure, UnsupportedOnGpu, ZeroFDiagonal
+from .errors import LinearSolveFailure, ZeroFDiagonal, ZeroPivot
+from .ilu import IluFactorization, ilu_factor
 from .krylov import GmresOptions, gmres
 from .mgr import cpr_specs, mgr_setup
 from .sparse import DeviceMatrix, abs_row_sum_max, as_device, equilibrate
@@ -58,8 +60,7 @@ class GmresSolver:
     """GMRES with a per-system GPU preconditioner (linsolve.py:46-73).
 
     preconditioner: 'mgr' (uses mgr_specs), 'cpr' (MGR in the CPR-emulation
-    configuration), 'none'; 'ilu' is validated like the reference but not
-    available on the GPU."""
+    configuration), 'ilu' (level ilu_level) or 'none'."""
 
     def __init__(self, preconditioner="none", gmres_opts: GmresOptions | None = None, mgr_specs=None,
                  amg_opts: AmgOptions | None = None, ilu_level: int = 0, post_smoothing: bool = False,
@@ -80,8 +81,10 @@ class GmresSolver:
         if self.preconditioner == "none":
             return None
         if self.preconditioner == "ilu":
-            raise UnsupportedOnGpu("GmresSolver(preconditioner='ilu') is the CPU ILU(k) comparator; "
-                                   "not available on the GPU path")
+            try:
+                return ilu_factor(a, self.ilu_level)
+            except ZeroPivot as err:
+                raise LinearSolveFailure(f"ILU({self.ilu_level}) setup failed: {err}") from err
         specs = self.mgr_specs if self.preconditioner == "mgr" else cpr_specs()
         if specs is None:
             raise ValueError("GmresSolver(preconditioner='mgr') needs mgr_specs")
@@ -102,9 +105,9 @@ class GmresSolver:
         if self.equilibrate:
             a, row, col_scale = equilibrate(a)
             rhs = rhs / row
-        hier = self._build_preconditioner(system, a)
+        pc = self._build_preconditioner(system, a)
         a_norm = abs_row_sum_max(a)
-        result = gmres(a, hier, rhs, self.gmres_opts, a_norm=a_norm)
+        result = gmres(a, pc, rhs, self.gmres_opts, a_norm=a_norm)
         x = result.x if col_scale is None else col_scale * result.x
         return LinearSolveResult(x=x, iterations=result.iterations, converged=result.converged,
                                  residual_norm=result.residual_norm)

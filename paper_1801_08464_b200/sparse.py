@@ -229,3 +229,19 @@ def abs_row_sum_max(a: DeviceMatrix) -> float:
     out = _lib.ctypes.c_double()
     a.ctx.call("mg_abs_row_sum_max", a.h, _lib.ctypes.byref(out))
     return float(out.value)
+
+
+# -- Matrix Market I/O (sparse.py:256-264) -------------------------------------
+def read_matrix_market(path, ctx=None) -> DeviceMatrix:
+    """Load a Matrix Market file (e.g. the Jacobians _DumpingSolver writes,
+    bench.py:286-300) straight into a device matrix."""
+    import scipy.io
+    import scipy.sparse as sp
+    return DeviceMatrix.from_host(sp.csr_matrix(scipy.io.mmread(path, spmatrix=False)), ctx)
+
+
+def write_matrix_market(path, a, comment=""):
+    """Write a device (or host) matrix as a Matrix Market coordinate file."""
+    import scipy.io
+    m = a.to_scipy() if isinstance(a, DeviceMatrix) else (a.m if hasattr(a, "m") else a)
+    scipy.io.mmwrite(path, m.tocoo(), comment=comment)
