@@ -22,43 +22,53 @@ static int red_blocks(int64_t n) {
 }
 
 __global__ void k_fill(double *x, double val, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = val;
 }
 __global__ void k_mul(double *y, const double *a, const double *x, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = a[i] * x[i];
 }
 __global__ void k_axpy(double *y, double a, const double *x, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = y[i] + a * x[i];
 }
 __global__ void k_add(double *y, const double *x, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = y[i] + x[i];
 }
 __global__ void k_divs(double *y, const double *x, double d, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = x[i] / d;
 }
 __global__ void k_sub(double *r, const double *b, const double *ax, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     r[i] = b[i] - ax[i];
 }
 __global__ void k_gather(double *d, const double *s, const int *idx, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = s[idx[i]];
 }
 __global__ void k_scatter_add(double *d, const double *s, const int *idx, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[idx[i]] = d[idx[i]] + s[i];
 }
 __global__ void k_scatter_set(double *d, const double *s, const int *idx, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[idx[i]] = s[i];
 }
 
 __global__ void k_fc_merge(double *e, const double *ef, const int *fmap, int64_t n) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int f = fmap[i];
     e[i] = f >= 0 ? ef[f] : 0.0;
@@ -69,54 +79,54 @@ static int ew_grid(int64_t n) { return grid_for(n, 256, g_ctx->num_sms * 8); }
 
 void fc_merge(double *e, const double *ef, const int *fmap, int64_t n) {
   if (!n) return;
-  k_fc_merge<<<ew_grid(n), 256, 0, stream()>>>(e, ef, fmap, n);
+  launch_pdl(k_fc_merge, ew_grid(n), 256, 0, e, ef, fmap, n);
   check_launch("fc_merge");
 }
 
 void vfill(double *x, double val, int64_t n) {
   if (!n) return;
-  k_fill<<<ew_grid(n), 256, 0, stream()>>>(x, val, n);
+  launch_pdl(k_fill, ew_grid(n), 256, 0, x, val, n);
   check_launch("fill");
 }
 void vcopy(double *dst, const double *src, int64_t n) { d2d(dst, src, n * sizeof(double)); }
 void vmul(double *y, const double *a, const double *x, int64_t n) {
   if (!n) return;
-  k_mul<<<ew_grid(n), 256, 0, stream()>>>(y, a, x, n);
+  launch_pdl(k_mul, ew_grid(n), 256, 0, y, a, x, n);
   check_launch("mul");
 }
 void vaxpy(double *y, double a, const double *x, int64_t n) {
   if (!n) return;
-  k_axpy<<<ew_grid(n), 256, 0, stream()>>>(y, a, x, n);
+  launch_pdl(k_axpy, ew_grid(n), 256, 0, y, a, x, n);
   check_launch("axpy");
 }
 void vadd(double *y, const double *x, int64_t n) {
   if (!n) return;
-  k_add<<<ew_grid(n), 256, 0, stream()>>>(y, x, n);
+  launch_pdl(k_add, ew_grid(n), 256, 0, y, x, n);
   check_launch("add");
 }
 void vdiv_scalar(double *y, const double *x, double d, int64_t n) {
   if (!n) return;
-  k_divs<<<ew_grid(n), 256, 0, stream()>>>(y, x, d, n);
+  launch_pdl(k_divs, ew_grid(n), 256, 0, y, x, d, n);
   check_launch("div");
 }
 void vsub(double *r, const double *b, const double *ax, int64_t n) {
   if (!n) return;
-  k_sub<<<ew_grid(n), 256, 0, stream()>>>(r, b, ax, n);
+  launch_pdl(k_sub, ew_grid(n), 256, 0, r, b, ax, n);
   check_launch("sub");
 }
 void gather(double *dst, const double *src, const int *idx, int64_t n) {
   if (!n) return;
-  k_gather<<<ew_grid(n), 256, 0, stream()>>>(dst, src, idx, n);
+  launch_pdl(k_gather, ew_grid(n), 256, 0, dst, src, idx, n);
   check_launch("gather");
 }
 void scatter_add(double *dst, const double *src, const int *idx, int64_t n) {
   if (!n) return;
-  k_scatter_add<<<ew_grid(n), 256, 0, stream()>>>(dst, src, idx, n);
+  launch_pdl(k_scatter_add, ew_grid(n), 256, 0, dst, src, idx, n);
   check_launch("scatter_add");
 }
 void scatter_set(double *dst, const double *src, const int *idx, int64_t n) {
   if (!n) return;
-  k_scatter_set<<<ew_grid(n), 256, 0, stream()>>>(dst, src, idx, n);
+  launch_pdl(k_scatter_set, ew_grid(n), 256, 0, dst, src, idx, n);
   check_launch("scatter_set");
 }
 
@@ -143,6 +153,7 @@ __device__ __forceinline__ void block_reduce_store(double (&acc)[KM], int K, dou
 
 // out[k] = sum_b partial[b*K + k], one warp per k, fixed order
 __global__ void k_finish(const double *partial, int nb, int K, double *out) {
+  PDL_ENTRY();
   int k = blockIdx.x;
   int lane = threadIdx.x;
   double s = 0.0;
@@ -153,6 +164,7 @@ __global__ void k_finish(const double *partial, int nb, int K, double *out) {
 }
 
 __global__ void __launch_bounds__(RB) k_dot(const double *x, const double *y, int64_t n, double *partial) {
+  PDL_ENTRY();
   double acc[1] = {0.0};
   for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
     acc[0] += x[i] * y[i];
@@ -160,7 +172,7 @@ __global__ void __launch_bounds__(RB) k_dot(const double *x, const double *y, in
 }
 
 static double reduce_finish(double *partial, int nb, int K, double *out_dev) {
-  k_finish<<<K, 32, 0, stream()>>>(partial, nb, K, out_dev);
+  launch_pdl(k_finish, K, 32, 0, partial, nb, K, out_dev);
   check_launch("finish");
   return 0.0;
 }
@@ -169,7 +181,7 @@ double dot(const double *x, const double *y, int64_t n) {
   int nb = red_blocks(n);
   double *part = red_scratch((size_t)nb + 8);
   double *out = part + nb;
-  k_dot<<<nb, RB, 0, stream()>>>(x, y, n, part);
+  launch_pdl(k_dot, nb, RB, 0, x, y, n, part);
   check_launch("dot");
   reduce_finish(part, nb, 1, out);
   double h = 0.0;
@@ -185,6 +197,7 @@ double nrm2(const double *x, int64_t n) { return sqrt(dot(x, x, n)); }
 static const int MCH = 2048;
 __global__ void __launch_bounds__(256) k_mdot2(const double *__restrict__ V, int64_t ldv, int K,
                                               const double *__restrict__ w, int64_t n, double *partial) {
+  PDL_ENTRY();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t c0 = (int64_t)blockIdx.x * MCH; c0 < n; c0 += (int64_t)gridDim.x * MCH) {
@@ -218,6 +231,7 @@ __global__ void __launch_bounds__(256) k_mdot2(const double *__restrict__ V, int
 // w -= sum_k c_k V_k (streaming, two elements per thread)
 __global__ void __launch_bounds__(RB) k_update(const double *__restrict__ V, int64_t ldv, int K,
                                               const double *__restrict__ c, double *w, int64_t n) {
+  PDL_ENTRY();
   __shared__ double cc[32];
   if (threadIdx.x < 32) cc[threadIdx.x] = (int)threadIdx.x < K ? c[threadIdx.x] : 0.0;
   __syncthreads();
@@ -238,6 +252,7 @@ __global__ void __launch_bounds__(RB) k_update(const double *__restrict__ V, int
 __global__ void __launch_bounds__(RB) k_update_norm(const double *__restrict__ V, int64_t ldv, int K,
                                                    const double *__restrict__ c, double *w, int64_t n,
                                                    double *partial) {
+  PDL_ENTRY();
   __shared__ double cc[32];
   if (threadIdx.x < 32) cc[threadIdx.x] = (int)threadIdx.x < K ? c[threadIdx.x] : 0.0;
   __syncthreads();
@@ -292,6 +307,7 @@ template <int KM>
 __global__ void __launch_bounds__(RB) k_combine(const double *__restrict__ V, int64_t ldv, int K,
                                                const double *__restrict__ y, double *u, int64_t n,
                                                int accumulate) {
+  PDL_ENTRY();
   double cc[KM];
 #pragma unroll
   for (int k = 0; k < KM; ++k) cc[k] = k < K ? y[k] : 0.0;
@@ -313,6 +329,7 @@ __global__ void __launch_bounds__(RB) k_combine(const double *__restrict__ V, in
 __global__ void __launch_bounds__(256) k_mdot2x(const double *__restrict__ V, int64_t ldv, int K,
                                                const double *__restrict__ u, const double *__restrict__ w,
                                                int64_t n, double *partial) {
+  PDL_ENTRY();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double au[4] = {0.0, 0.0, 0.0, 0.0}, aw[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t c0 = (int64_t)blockIdx.x * MCH; c0 < n; c0 += (int64_t)gridDim.x * MCH) {
@@ -364,6 +381,7 @@ __global__ void __launch_bounds__(RB) k_dcgs2_update(double *V, int64_t ldv, int
                                                     const double *__restrict__ coef,
                                                     const double *__restrict__ w, int64_t n,
                                                     double *partial) {
+  PDL_ENTRY();
   __shared__ double cs[32], ce[32], sc[3];
   if (threadIdx.x < 32) {
     cs[threadIdx.x] = (int)threadIdx.x < j ? coef[threadIdx.x] : 0.0;
@@ -402,7 +420,7 @@ void mdot2x(const double *V, int64_t ldv, int K, const double *u, const double *
   int64_t cap = (int64_t)g_ctx->num_sms * 8 * (8 / nw);
   int nb = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   double *part = red_scratch((size_t)nb * 64);
-  k_mdot2x<<<nb, 32 * nw, 0, stream()>>>(V, ldv, K, u, w, n, part);
+  launch_pdl(k_mdot2x, nb, 32 * nw, 0, V, ldv, K, u, w, n, part);
   check_launch("mdot2x");
   reduce_finish(part, nb, 2 * K, out_dev);
 }
@@ -412,7 +430,7 @@ void dcgs2_update(double *V, int64_t ldv, int j, const double *coef_dev, const d
   if (j > 32) throw MgError(MG_ERR_UNSUPPORTED, "dcgs2_update: at most 32 vectors");
   int nb = red_blocks(n);
   double *part = red_scratch((size_t)nb + 8);
-  k_dcgs2_update<<<nb, RB, 0, stream()>>>(V, ldv, j, coef_dev, w, n, part);
+  launch_pdl(k_dcgs2_update, nb, RB, 0, V, ldv, j, coef_dev, w, n, part);
   check_launch("dcgs2_update");
   reduce_finish(part, nb, 1, norm2_dev);
 }
@@ -427,7 +445,7 @@ void mdot(const double *V, int64_t ldv, int K, const double *w, int64_t n, doubl
     int kk = K - k0 < 32 ? K - k0 : 32;
     double *part = red_scratch((size_t)nb * 32);
     const double *Vk = V + (int64_t)k0 * ldv;
-    k_mdot2<<<nb, 256, 0, stream()>>>(Vk, ldv, kk, w, n, part);
+    launch_pdl(k_mdot2, nb, 256, 0, Vk, ldv, kk, w, n, part);
     check_launch("mdot");
     reduce_finish(part, nb, kk, out_dev + k0);
   }
@@ -437,7 +455,7 @@ void update_mdot(const double *V, int64_t ldv, int K, const double *c_dev, doubl
                  double *out_dev) {
   if (K <= 32) {
     // w -= cV (one streaming pass), then the projections of the updated w
-    k_update<<<grid_for(n, RB, g_ctx->num_sms * 8), RB, 0, stream()>>>(V, ldv, K, c_dev, w, n);
+    launch_pdl(k_update, grid_for(n, RB, g_ctx->num_sms * 8), RB, 0, V, ldv, K, c_dev, w, n);
     check_launch("update");
     mdot(V, ldv, K, w, n, out_dev);
     return;
@@ -454,7 +472,7 @@ void update_norm2(const double *V, int64_t ldv, int K, const double *c_dev, doub
   int nb = red_blocks(n);
   double *part = red_scratch((size_t)nb + 8);
   if (K <= 32) {
-    k_update_norm<<<nb, RB, 0, stream()>>>(V, ldv, K, c_dev, w, n, part);
+    launch_pdl(k_update_norm, nb, RB, 0, V, ldv, K, c_dev, w, n, part);
     check_launch("update_norm");
     reduce_finish(part, nb, 1, out_dev);
     return;
@@ -462,7 +480,7 @@ void update_norm2(const double *V, int64_t ldv, int K, const double *c_dev, doub
   DBuf<double> t((size_t)n);
   combine(V, ldv, K, c_dev, t.p, n);
   vaxpy(w, -1.0, t.p, n);
-  k_dot<<<nb, RB, 0, stream()>>>(w, w, n, part);
+  launch_pdl(k_dot, nb, RB, 0, w, w, n, part);
   check_launch("dot");
   reduce_finish(part, nb, 1, out_dev);
 }
@@ -473,8 +491,8 @@ void combine(const double *V, int64_t ldv, int K, const double *y_dev, double *u
   for (int k0 = 0; k0 < K; k0 += 32) {
     int kk = K - k0 < 32 ? K - k0 : 32;
     const double *Vk = V + (int64_t)k0 * ldv;
-    KSEL(kk, (k_combine<16><<<nb, RB, 0, stream()>>>(Vk, ldv, kk, y_dev + k0, u, n, k0 > 0)),
-         (k_combine<32><<<nb, RB, 0, stream()>>>(Vk, ldv, kk, y_dev + k0, u, n, k0 > 0)));
+    KSEL(kk, (launch_pdl(k_combine<16>, nb, RB, 0, Vk, ldv, kk, y_dev + k0, u, n, k0 > 0)),
+         (launch_pdl(k_combine<32>, nb, RB, 0, Vk, ldv, kk, y_dev + k0, u, n, k0 > 0)));
     check_launch("combine");
   }
 }

@@ -125,6 +125,7 @@ __global__ void k_scale_rows(int N, const int *rp, const int *ci, const double *
 template <int B>
 __global__ void k_block_apply(int N, const double *__restrict__ dinv, const double *__restrict__ x,
                               double *__restrict__ z) {
+  PDL_ENTRY();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   double d[B * B], xv[B];
@@ -190,9 +191,9 @@ void block_apply(const Csr &dinv, const double *x, double *z) {
   int N = dinv.nr;
   if (!N) return;
   if (dinv.b == 2)
-    k_block_apply<2><<<grid_for(N, 256), 256, 0, stream()>>>(N, dinv.v.p, x, z);
+    launch_pdl(k_block_apply<2>, grid_for(N, 256), 256, 0, N, dinv.v.p, x, z);
   else if (dinv.b == 3)
-    k_block_apply<3><<<grid_for(N, 256), 256, 0, stream()>>>(N, dinv.v.p, x, z);
+    launch_pdl(k_block_apply<3>, grid_for(N, 256), 256, 0, N, dinv.v.p, x, z);
   else
     throw MgError(MG_ERR_UNSUPPORTED, "block_apply: b must be 2 or 3");
   check_launch("block_apply");

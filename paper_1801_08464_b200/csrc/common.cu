@@ -209,6 +209,15 @@ void sync() {
   MG_CUDA(cudaStreamSynchronize(g_ctx->stream));
 }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_PDL");
+    on = !(e && *e == '0');
+  }
+  return on;
+}
+
 bool trace_on() {
   if (g_ctx && g_ctx->owner) return false;  // worker threads do not trace
   static int on = -1;

@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <utility>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -101,6 +102,37 @@ class TaskGroup {
 void alloc_release_cache(Ctx *c);
 
 inline cudaStream_t stream() { return g_ctx->stream; }
+
+// ---- programmatic dependent launch (PDL) -------------------------------------------
+// Solve-phase kernels are launched with programmatic stream serialisation: the
+// next kernel's launch (and CTA scheduling) overlaps this kernel's tail instead
+// of waiting for the grid to drain.  Every kernel launched this way calls
+// pdl_wait() before its first global memory access (it returns once every
+// predecessor grid has completed and its writes are visible), and
+// pdl_trigger() right after, so that its own successor may start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define PDL_ENTRY() \
+  do {              \
+    pdl_wait();     \
+    pdl_trigger();  \
+  } while (0)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw MgError(MG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
 inline void count_launch(int n = 1) { g_ctx->launches += n; }
 inline void check_launch(const char *what) {
   cudaError_t e = cudaGetLastError();

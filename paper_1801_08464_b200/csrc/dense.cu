@@ -175,6 +175,7 @@ int dense_inverse(const double *a_dev, double *inv_dev, int n) {
 
 // y = M x, one warp per row
 __global__ void k_dense_mv(const double *__restrict__ m, const double *__restrict__ x, double *y, int n) {
+  PDL_ENTRY();
   int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   double s = 0.0;
@@ -186,7 +187,7 @@ __global__ void k_dense_mv(const double *__restrict__ m, const double *__restric
 
 void dense_matvec(const double *m_dev, const double *x, double *y, int n) {
   if (!n) return;
-  k_dense_mv<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(m_dev, x, y, n);
+  launch_pdl(k_dense_mv, grid_for((int64_t)n * 32, 256), 256, 0, m_dev, x, y, n);
   check_launch("dense_mv");
 }
 

@@ -299,6 +299,7 @@ static void fsolve(FSolver &fs, const Csr &aff, const double *r, double *x) {
 // per-cell block-diagonal relaxation: x[id] = inv_b r[id] per block
 __global__ void k_bd_apply(int nblk, const int *ioff, const int64_t *moff, const int *idx, const double *inv,
                            const double *r, double *x) {
+  PDL_ENTRY();
   int bi = blockIdx.x * blockDim.x + threadIdx.x;
   if (bi >= nblk) return;
   const int k = ioff[bi + 1] - ioff[bi];
@@ -536,7 +537,7 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
   bool zero = true;
   bool f_only = false;  // e = [e_F; 0] exactly (F-relaxation from zero)
   if (lv.bd) {
-    k_bd_apply<<<grid_for(lv.bd->nblk, 128), 128, 0, stream()>>>(lv.bd->nblk, lv.bd->ioff.p, lv.bd->moff.p,
+    launch_pdl(k_bd_apply, grid_for(lv.bd->nblk, 128), 128, 0, lv.bd->nblk, lv.bd->ioff.p, lv.bd->moff.p,
                                                                  lv.bd->idx.p, lv.bd->inv.p, r, e);
     check_launch("bd_apply");
     zero = false;

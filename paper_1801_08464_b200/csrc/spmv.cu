@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ row
                                              const int *__restrict__ ci,
                                              const double *__restrict__ v,
                                              const double *__restrict__ x, Epi epi) {
+  PDL_ENTRY();
   const int lane = threadIdx.x % VS;
   const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VS);
   const int ng = (int)((int64_t)gridDim.x * blockDim.x / VS);
@@ -74,6 +75,7 @@ template <int UNR, class Epi>
 __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sptr, const int *__restrict__ rlen,
                                               const int *__restrict__ ci, const double *__restrict__ v,
                                               const double *__restrict__ x, Epi epi) {
+  PDL_ENTRY();
   int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= nr) return;
   const int base = __ldg(sptr + (row >> 5)) + (row & 31);
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(256) k_bsr(int nbr, const int *__restrict__ rp
                                              const double *__restrict__ v,
                                              const double *__restrict__ x,
                                              double *__restrict__ y) {
+  PDL_ENTRY();
   const int lane = threadIdx.x % G;
   const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G);
   const int ng = (int)((int64_t)gridDim.x * blockDim.x / G);
@@ -295,21 +298,21 @@ static void launch_csr(const Csr &a, const double *x, Epi epi) {
   cudaStream_t s = stream();
   (void)T;
 #define LAUNCH_AVG(VS, U) \
-  k_csr<VS, U, Epi><<<spmv_grid((int64_t)a.nr * VS), 256, 0, s>>>(a.nr, nullptr, a.rp.p, a.ci.p, a.v.p, x, epi)
+  launch_pdl(k_csr<VS, U, Epi>, spmv_grid((int64_t)a.nr * VS), 256, 0, a.nr, nullptr, a.rp.p, a.ci.p, a.v.p, x, epi)
   prepare_spmv(a);
   const SpmvPlan &pl = *a.plan;
   if (pl.sell) {
     if (avg > 64)
-      k_sell<8, Epi><<<grid_for(a.nr, 128), 128, 0, s>>>(a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
+      launch_pdl(k_sell<8, Epi>, grid_for(a.nr, 128), 128, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
     else
-      k_sell<4, Epi><<<grid_for(a.nr, 256), 256, 0, s>>>(a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
+      launch_pdl(k_sell<4, Epi>, grid_for(a.nr, 256), 256, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
     check_launch("sell spmv");
     return;
   }
   auto run = [&](int c, int n, const int *rows) {
     if (!n) return;
 #define LAUNCH(VS, U) \
-  k_csr<VS, U, Epi><<<spmv_grid((int64_t)n * VS), 256, 0, s>>>(n, rows, a.rp.p, a.ci.p, a.v.p, x, epi)
+  launch_pdl(k_csr<VS, U, Epi>, spmv_grid((int64_t)n * VS), 256, 0, n, rows, a.rp.p, a.ci.p, a.v.p, x, epi)
     switch (c) {
       case 0: LAUNCH(1, 2); break;
       case 1: LAUNCH(2, 3); break;
@@ -352,11 +355,11 @@ void spmv(const Csr &a, const double *x, double *y) {
   cudaStream_t s = stream();
   (void)T;
   if (a.b == 2) {
-    if (avg <= 4.5) k_bsr<2, 2, 3><<<spmv_grid((int64_t)a.nr * 2), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
-    else k_bsr<2, 4, 2><<<spmv_grid((int64_t)a.nr * 4), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    if (avg <= 4.5) launch_pdl(k_bsr<2, 2, 3>, spmv_grid((int64_t)a.nr * 2), 256, 0, a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    else launch_pdl(k_bsr<2, 4, 2>, spmv_grid((int64_t)a.nr * 4), 256, 0, a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
   } else if (a.b == 3) {
-    if (avg <= 4.5) k_bsr<3, 2, 3><<<spmv_grid((int64_t)a.nr * 2), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
-    else k_bsr<3, 4, 2><<<spmv_grid((int64_t)a.nr * 4), 256, 0, s>>>(a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    if (avg <= 4.5) launch_pdl(k_bsr<3, 2, 3>, spmv_grid((int64_t)a.nr * 2), 256, 0, a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
+    else launch_pdl(k_bsr<3, 4, 2>, spmv_grid((int64_t)a.nr * 4), 256, 0, a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
   } else {
     throw MgError(MG_ERR_UNSUPPORTED, "block size must be 1, 2 or 3");
   }
