@@ -13,6 +13,8 @@ void spmv(const Csr &a, const double *x, double *y);
 void residual(const Csr &a, const double *x, const double *b, double *r);
 // y = y + A x
 void spmv_add(const Csr &a, const double *x, double *y);
+// y = [ef scattered by fmap (fmap[i] < 0: 0)] + A x
+void spmv_merge_add(const Csr &a, const double *x, const int *fmap, const double *ef, double *y);
 // xo = x + dinv .* (b - A x)   (L1-Jacobi sweep)
 void jacobi_sweep(const Csr &a, const double *x, const double *b, const double *dinv, double *xo);
 

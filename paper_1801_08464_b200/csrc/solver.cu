@@ -536,6 +536,7 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
   MgrLevel &lv = h.L[k];
   bool zero = true;
   bool f_only = false;  // e = [e_F; 0] exactly (F-relaxation from zero)
+  bool merged = true;   // false: e = [e_F; 0] not written yet (merged into the prolongation)
   if (lv.bd) {
     launch_pdl(k_bd_apply, grid_for(lv.bd->nblk, 128), 128, 0, lv.bd->nblk, lv.bd->ioff.p, lv.bd->moff.p,
                                                                  lv.bd->idx.p, lv.bd->inv.p, r, e);
@@ -560,7 +561,10 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
     }
     ProfScope ps(4);
     if (zero) {
-      fc_merge(e, lv.eF.p, lv.fmap.p, lv.n);  // e = [e_F; 0] in one pass
+      // e = [e_F; 0]: with A[:, F] the residual reads e_F directly and the merge
+      // is folded into the prolongation's epilogue; otherwise one merge pass
+      if (lv.AF.nr && !h.post_smoothing) merged = false;
+      else fc_merge(e, lv.eF.p, lv.fmap.p, lv.n);
       f_only = true;
     } else {
       scatter_add(e, lv.eF.p, lv.flist.p, lv.nf);
@@ -577,7 +581,9 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
     apply_level(h, k + 1, lv.rc.p, lv.ec.p);
     ProfScope ps(4);
     if (zero) spmv(lv.P, lv.ec.p, e);
+    else if (!merged) spmv_merge_add(lv.P, lv.ec.p, lv.fmap.p, lv.eF.p, e);
     else spmv_add(lv.P, lv.ec.p, e);
+    merged = true;
     zero = false;
     f_only = false;
   };

@@ -23,6 +23,17 @@ struct EpiAdd {
   double *y;
   __device__ void operator()(int r, double s) const { y[r] = y[r] + s; }
 };
+// y = [e_F; 0] + A x with the F values merged on the fly (MGR prolongation after
+// an F-relaxation from zero: replaces fc_merge + y += A x, same sums)
+struct EpiMergeAdd {
+  const int *fmap;
+  const double *ef;
+  double *y;
+  __device__ void operator()(int r, double s) const {
+    const int f = fmap[r];
+    y[r] = (f >= 0 ? ef[f] : 0.0) + s;
+  }
+};
 struct EpiJacobi {
   const double *x, *b, *dinv;
   double *xo;
@@ -369,6 +380,11 @@ void spmv(const Csr &a, const double *x, double *y) {
 void residual(const Csr &a, const double *x, const double *b, double *r) {
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "residual: scalar CSR only");
   launch_csr(a, x, EpiResid{b, r});
+}
+
+void spmv_merge_add(const Csr &a, const double *x, const int *fmap, const double *ef, double *y) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spmv_merge_add: scalar CSR only");
+  launch_csr(a, x, EpiMergeAdd{fmap, ef, y});
 }
 
 void spmv_add(const Csr &a, const double *x, double *y) {
