@@ -114,8 +114,11 @@ def peaks():
 
 def cpu_baseline(edge, config, seconds=10.0):
     """Oracle port (numpy/scipy + C restatement) on one host core, bounded sample."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    try:  # numpy is already loaded: limit its BLAS pool to the one core reported
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(1)
+    except Exception:  # noqa: BLE001
+        limiter = None
     from oracle import pipeline as opipe
     from oracle import amg as oamg, mgr as omgr
     from paper_1801_08464_b200 import pipeline as gpipe, synth
@@ -132,6 +135,8 @@ def cpu_baseline(edge, config, seconds=10.0):
         if time.perf_counter() - t0 >= seconds:
             break
     el = time.perf_counter() - t0
+    if limiter is not None:
+        limiter.restore_original_limits()
     return {"value": dofs / el, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"config-{config} generator at {edge}^3 ({s.n} DOFs), {runs} solve(s) in {el:.1f}s, "
                       f"{its[-1]} GMRES its, oracle (numpy/scipy + C restatement)"}
@@ -143,10 +148,15 @@ def reference_arm(args, ws, rank):
     if rank != 0:
         return
     import multiprocessing as mp
-    ncpu = os.cpu_count() or 1
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     from paper_1801_08464_b200 import synth
     n = synth.make_config(args.config, cfg_edge).n
-    ctxmp = mp.get_context("fork")
+    # one single-threaded BLAS per worker process (spawned: the limits apply
+    # before numpy loads; forked workers inherited the parent's thread pools and
+    # oversubscribed the cores)
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
+    ctxmp = mp.get_context("spawn")
     with ctxmp.Pool(ncpu) as pool:
         for _ in range(args.warmup if args.warmup < 1 else 1):
             pool.map(_ref_one, [(args.config, cfg_edge)] * ncpu)
@@ -170,8 +180,12 @@ def reference_arm(args, ws, rank):
 
 
 def _ref_one(a):
-    os.environ["OMP_NUM_THREADS"] = "1"
     cfg, edge = a
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:  # noqa: BLE001
+        pass
     from oracle import pipeline as opipe
     from oracle import amg as oamg, mgr as omgr
     from paper_1801_08464_b200 import pipeline as gpipe, synth
