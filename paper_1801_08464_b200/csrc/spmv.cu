@@ -193,8 +193,122 @@ __global__ void k_cls_fill(int n, const int *rp, int *fill, int *rows) {
   if (c >= 0) rows[base[c] + r] = i;
 }
 
+// ---- block SELL-32 for the BCSR GMRES operator -------------------------------------
+// slices of 32 block rows, block k of the slice's rows contiguous (32 b*b blocks),
+// one thread per block row: every block load is a coalesced 1 KB (b = 2) warp access
+template <int B>
+__global__ void k_bsell_fill(int nr, const int *rp, const int *ci, const double *v, const int *sptr, int *sci,
+                             double *sv) {
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nr) return;
+  int base = sptr[row >> 5] + (row & 31);
+  int s = rp[row], e = rp[row + 1];
+  for (int k = 0; k < e - s; ++k) {
+    sci[base + k * 32] = ci[s + k];
+#pragma unroll
+    for (int q = 0; q < B * B; ++q) sv[(int64_t)(base + k * 32) * B * B + q] = v[(int64_t)(s + k) * B * B + q];
+  }
+}
+
+template <int B, int UNR>
+__global__ void __launch_bounds__(256) k_bsell(int nr, const int *__restrict__ sptr, const int *__restrict__ rlen,
+                                               const int *__restrict__ ci, const double *__restrict__ v,
+                                               const double *__restrict__ x, double *__restrict__ y) {
+  PDL_ENTRY();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nr) return;
+  const int base = __ldg(sptr + (row >> 5)) + (row & 31);
+  const int len = __ldg(rlen + row);
+  double acc[B];
+#pragma unroll
+  for (int r = 0; r < B; ++r) acc[r] = 0.0;
+  for (int k0 = 0; k0 < len; k0 += UNR) {
+    double a[UNR][B * B], xc[UNR][B];
+    int cc[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int k = k0 + u;
+      const int e = base + (k < len ? k : 0) * 32;
+      cc[u] = k < len ? __ldcs(ci + e) : -1;
+      if (B == 2) {
+        const double2 *vb = reinterpret_cast<const double2 *>(v) + (int64_t)e * 2;
+        double2 r0 = __ldcs(vb), r1 = __ldcs(vb + 1);
+        a[u][0] = r0.x; a[u][1] = r0.y; a[u][2] = r1.x; a[u][3] = r1.y;
+      } else {
+#pragma unroll
+        for (int q = 0; q < B * B; ++q) a[u][q] = __ldcs(v + (int64_t)e * B * B + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (cc[u] < 0) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) xc[u][q] = 0.0;
+        continue;
+      }
+      if (B == 2) {
+        double2 t = __ldg(reinterpret_cast<const double2 *>(x) + cc[u]);
+        xc[u][0] = t.x; xc[u][1] = t.y;
+      } else {
+#pragma unroll
+        for (int q = 0; q < B; ++q) xc[u][q] = __ldg(x + (int64_t)cc[u] * B + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (cc[u] < 0) continue;
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < B; ++q) t += a[u][r * B + q] * xc[u][q];
+        acc[r] += t;
+      }
+    }
+  }
+  if (B == 2) {
+    reinterpret_cast<double2 *>(y)[row] = make_double2(acc[0], acc[1]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < B; ++r) y[(int64_t)row * B + r] = acc[r];
+  }
+}
+
+static void build_bsell(const Csr &a, SpmvPlan &pl) {
+  const int B = a.b;
+  int ns = (a.nr + 31) / 32;
+  DBuf<int> slen((size_t)ns + 1);
+  pl.rlen.alloc(a.nr);
+  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p);
+  check_launch("bsell_len");
+  DBuf<int64_t> sp64((size_t)ns + 1);
+  int64_t padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
+  if (padded > 2 * a.nnz + 4096 || padded * B * B > 2000000000LL) {
+    pl.rlen.release();
+    return;
+  }
+  pl.sptr.alloc((size_t)ns + 1);
+  exclusive_scan_i32_to_i32(slen.p, pl.sptr.p, ns);
+  pl.sci.alloc((size_t)padded);
+  pl.sv.alloc((size_t)padded * B * B);
+  if (B == 2)
+    k_bsell_fill<2><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, pl.sptr.p, pl.sci.p,
+                                                               pl.sv.p);
+  else
+    k_bsell_fill<3><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, pl.sptr.p, pl.sci.p,
+                                                               pl.sv.p);
+  check_launch("bsell_fill");
+  pl.sell = true;
+}
+
 void prepare_spmv(const Csr &a) {
-  if (a.plan || a.b != 1) return;
+  if (a.plan) return;
+  if (a.b != 1) {  // block CSR (the GMRES operator): block SELL copy when large
+    auto pl = std::make_unique<SpmvPlan>();
+    if ((a.b == 2 || a.b == 3) && a.nr >= 32768) build_bsell(a, *pl);
+    a.plan = std::move(pl);
+    return;
+  }
   auto pl = std::make_unique<SpmvPlan>();
   const int NC = SpmvPlan::NC;
   if (a.nr > 0) {
@@ -355,6 +469,15 @@ static void launch_csr(const Csr &a, const double *x, Epi epi) {
   for (int c = 0; c < SpmvPlan::NC; ++c) run(c, pl.cnt[c], pl.rows.p + pl.off[c]);
 }
 
+static bool bsell_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_BSELL");
+    on = !(e && *e == '0');
+  }
+  return on;
+}
+
 void spmv(const Csr &a, const double *x, double *y) {
   if (a.b == 1) {
     launch_csr(a, x, EpiStore{y});
@@ -365,6 +488,14 @@ void spmv(const Csr &a, const double *x, double *y) {
   double avg = (double)a.nnz / a.nr;
   cudaStream_t s = stream();
   (void)T;
+  prepare_spmv(a);
+  if (a.plan->sell && bsell_enabled()) {
+    const SpmvPlan &pl = *a.plan;
+    if (a.b == 2) launch_pdl(k_bsell<2, 4>, grid_for(a.nr, 256), 256, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, y);
+    else launch_pdl(k_bsell<3, 2>, grid_for(a.nr, 256), 256, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, y);
+    check_launch("bsell spmv");
+    return;
+  }
   if (a.b == 2) {
     if (avg <= 4.5) launch_pdl(k_bsr<2, 2, 3>, spmv_grid((int64_t)a.nr * 2), 256, 0, a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
     else launch_pdl(k_bsr<2, 4, 2>, spmv_grid((int64_t)a.nr * 4), 256, 0, a.nr, a.rp.p, a.ci.p, a.v.p, x, y);
