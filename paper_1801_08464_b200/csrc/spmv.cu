@@ -131,6 +131,15 @@ __global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *
   }
 }
 
+static double sell_min_avg() {
+  static double v = -1.0;
+  if (v < 0) {
+    const char *e = getenv("MG_SELL_MIN_AVG");
+    v = e ? atof(e) : 3.0;
+  }
+  return v;
+}
+
 static void build_sell(const Csr &a, SpmvPlan &pl) {
   int ns = (a.nr + 31) / 32;
   DBuf<int> slen((size_t)ns + 1);
@@ -149,7 +158,12 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
     const char *e = getenv("MG_SELL_CAP_LONG");
     cap_long = e ? atof(e) : 1.15;
   }
-  double cap = avg <= 16.0 ? 2.0 : cap_long;
+  static double cap_short = -1.0;
+  if (cap_short < 0) {
+    const char *e = getenv("MG_SELL_CAP_SHORT");
+    cap_short = e ? atof(e) : 2.0;
+  }
+  double cap = avg <= 16.0 ? cap_short : cap_long;
   if (padded > (int64_t)(cap * (double)a.nnz) + 4096 || padded > 2000000000LL) {
     pl.rlen.release();
     return;
@@ -332,7 +346,7 @@ void prepare_spmv(const Csr &a) {
       k_cls_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, cnt.p, pl->rows.p);
       check_launch("cls_fill");
     }
-    if (a.nr >= 32768 && a.nnz >= 3 * (int64_t)a.nr) build_sell(a, *pl);
+    if (a.nr >= 32768 && (double)a.nnz >= sell_min_avg() * a.nr) build_sell(a, *pl);
   }
   a.plan = std::move(pl);
 }
