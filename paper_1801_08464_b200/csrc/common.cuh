@@ -176,18 +176,12 @@ struct DBuf {
   T *get() const { return p; }
 };
 
-// SpMV launch plan of a scalar CSR: rows binned by length class so bimodal
-// matrices (identity rows of gas-absent cells next to ~60-entry Schur rows)
-// get a lane-group size per class (spmv.cu prepare_spmv).
+// SpMV launch plan of a matrix: a SELL-32 copy (scalar CSR) or block SELL-32
+// copy (BCSR) built once at setup when it pays (spmv.cu prepare_spmv).
 struct SpmvPlan {
-  static const int NC = 7;
-  bool binned = false;
-  int single = 0;            // class used when not binned
-  int cnt[NC] = {}, off[NC] = {};
-  DBuf<int> rows;            // row lists grouped by class
   // SELL-32 copy (slices of 32 consecutive rows, column-major inside a slice):
   // one thread per row, coalesced value/column loads and x gathers that
-  // coalesce across neighbouring stencil rows.  Built when padding <= 15%.
+  // coalesce across neighbouring stencil rows (padding caps in build_sell).
   bool sell = false;
   DBuf<int> sptr;            // slice start (elements), nslices + 1
   DBuf<int> rlen;            // row lengths

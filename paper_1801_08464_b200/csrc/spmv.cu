@@ -40,16 +40,21 @@ struct EpiJacobi {
   __device__ void operator()(int i, double s) const { xo[i] = x[i] + dinv[i] * (b[i] - s); }
 };
 
+// x gather functor of the SpMV kernels
+struct XPlain {
+  const double *x;
+  __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
+};
 // VS lanes cooperate on one row; each lane keeps U independent (value, column)
 // loads in flight before the dependent x gathers, so a warp has VS*U*12 B of
 // matrix traffic outstanding per round trip.  Groups stride over rows (grid
 // sized to the resident capacity); every lane runs the shuffle (uniform loop).
-template <int VS, int U, class Epi>
+template <int VS, int U, class Epi, class XG>
 __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ rows,
                                              const int *__restrict__ rp,
                                              const int *__restrict__ ci,
                                              const double *__restrict__ v,
-                                             const double *__restrict__ x, Epi epi) {
+                                             XG x, Epi epi) {
   PDL_ENTRY();
   const int lane = threadIdx.x % VS;
   const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VS);
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ row
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (cc[u] >= 0) sum += vv[u] * __ldg(x + cc[u]);
+          if (cc[u] >= 0) sum += vv[u] * x(cc[u]);
       }
     }
 #pragma unroll
@@ -82,10 +87,10 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ row
 }
 
 // ---- SELL-32: one thread per row, loads coalesced across the 32 rows of a slice ----
-template <int UNR, class Epi>
+template <int UNR, class Epi, class XG>
 __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sptr, const int *__restrict__ rlen,
                                               const int *__restrict__ ci, const double *__restrict__ v,
-                                              const double *__restrict__ x, Epi epi) {
+                                              XG x, Epi epi) {
   PDL_ENTRY();
   int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= nr) return;
@@ -102,9 +107,9 @@ __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sp
       cc[u] = __ldcs(ci + base + (k + u) * 32);
     }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) sum += vv[u] * __ldg(x + cc[u]);
+    for (int u = 0; u < UNR; ++u) sum += vv[u] * x(cc[u]);
   }
-  for (; k < len; ++k) sum += __ldcs(v + base + k * 32) * __ldg(x + __ldcs(ci + base + k * 32));
+  for (; k < len; ++k) sum += __ldcs(v + base + k * 32) * x(__ldcs(ci + base + k * 32));
   epi(row, sum);
 }
 
@@ -175,36 +180,6 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   k_sell_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, pl.sptr.p, pl.sci.p, pl.sv.p);
   check_launch("sell_fill");
   pl.sell = true;
-}
-
-// ---- SpMV plan: rows binned by length class ---------------------------------------
-// class c: len <= 2, 6, 12, 24, 48, 96, >96  ->  (VS, U) below
-__device__ __forceinline__ int len_class(int len) {
-  return len <= 2 ? 0 : len <= 6 ? 1 : len <= 12 ? 2 : len <= 24 ? 3 : len <= 48 ? 4 : len <= 96 ? 5 : 6;
-}
-__global__ void k_cls_count(int n, const int *rp, int *cnt) {
-  __shared__ int h[SpmvPlan::NC];
-  if (threadIdx.x < SpmvPlan::NC) h[threadIdx.x] = 0;
-  __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicAdd(&h[len_class(rp[i + 1] - rp[i])], 1);
-  __syncthreads();
-  if (threadIdx.x < SpmvPlan::NC && h[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], h[threadIdx.x]);
-}
-__global__ void k_cls_fill(int n, const int *rp, int *fill, int *rows) {
-  __shared__ int h[SpmvPlan::NC], base[SpmvPlan::NC];
-  if (threadIdx.x < SpmvPlan::NC) h[threadIdx.x] = 0;
-  __syncthreads();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  int c = -1, r = 0;
-  if (i < n) {
-    c = len_class(rp[i + 1] - rp[i]);
-    r = atomicAdd(&h[c], 1);
-  }
-  __syncthreads();
-  if (threadIdx.x < SpmvPlan::NC && h[threadIdx.x]) base[threadIdx.x] = atomicAdd(&fill[threadIdx.x], h[threadIdx.x]);
-  __syncthreads();
-  if (c >= 0) rows[base[c] + r] = i;
 }
 
 // ---- block SELL-32 for the BCSR GMRES operator -------------------------------------
@@ -324,30 +299,7 @@ void prepare_spmv(const Csr &a) {
     return;
   }
   auto pl = std::make_unique<SpmvPlan>();
-  const int NC = SpmvPlan::NC;
-  if (a.nr > 0) {
-    DBuf<int> cnt(NC);
-    dzero(cnt.p, sizeof(int) * NC);
-    k_cls_count<<<grid_for(a.nr, 256, g_ctx->num_sms * 4), 256, 0, stream()>>>(a.nr, a.rp.p, cnt.p);
-    check_launch("cls_count");
-    d2h(pl->cnt, cnt.p, sizeof(int) * NC);
-    int best = 0;
-    for (int c = 1; c < NC; ++c)
-      if (pl->cnt[c] > pl->cnt[best]) best = c;
-    pl->single = best;
-    // per-class binning is kept for experiments but off: measured slower on the
-    // config-3 hierarchy (row-list indirection = one more dependent load per row)
-    const bool enable_binning = false;
-    if (enable_binning && a.nr >= 4096 && pl->cnt[best] < 0.92 * a.nr) {
-      pl->binned = true;
-      for (int c = 1; c < NC; ++c) pl->off[c] = pl->off[c - 1] + pl->cnt[c - 1];
-      h2d(cnt.p, pl->off, sizeof(int) * NC);
-      pl->rows.alloc(a.nr);
-      k_cls_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, cnt.p, pl->rows.p);
-      check_launch("cls_fill");
-    }
-    if (a.nr >= 32768 && (double)a.nnz >= sell_min_avg() * a.nr) build_sell(a, *pl);
-  }
+  if (a.nr >= 32768 && (double)a.nnz >= sell_min_avg() * a.nr) build_sell(a, *pl);
   a.plan = std::move(pl);
 }
 
@@ -429,58 +381,38 @@ static int spmv_grid(int64_t threads_needed) {
   return (int)(want < 1 ? 1 : want);
 }
 
-template <class Epi>
-static void launch_csr(const Csr &a, const double *x, Epi epi) {
+template <class Epi, class XG = XPlain>
+static void launch_csr(const Csr &a, XG x, Epi epi) {
   if (a.nr == 0) return;
   double avg = a.nr ? (double)a.nnz / a.nr : 0.0;
-  const int T = 256;
-  cudaStream_t s = stream();
-  (void)T;
 #define LAUNCH_AVG(VS, U) \
-  launch_pdl(k_csr<VS, U, Epi>, spmv_grid((int64_t)a.nr * VS), 256, 0, a.nr, nullptr, a.rp.p, a.ci.p, a.v.p, x, epi)
+  launch_pdl(k_csr<VS, U, Epi, XG>, spmv_grid((int64_t)a.nr * VS), 256, 0, a.nr, nullptr, a.rp.p, a.ci.p, a.v.p, x, epi)
   prepare_spmv(a);
   const SpmvPlan &pl = *a.plan;
   if (pl.sell) {
     if (avg > 64)
-      launch_pdl(k_sell<8, Epi>, grid_for(a.nr, 128), 128, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
+      launch_pdl(k_sell<8, Epi, XG>, grid_for(a.nr, 128), 128, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x,
+                 epi);
     else
-      launch_pdl(k_sell<4, Epi>, grid_for(a.nr, 256), 256, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x, epi);
+      launch_pdl(k_sell<4, Epi, XG>, grid_for(a.nr, 256), 256, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x,
+                 epi);
     check_launch("sell spmv");
     return;
   }
-  auto run = [&](int c, int n, const int *rows) {
-    if (!n) return;
-#define LAUNCH(VS, U) \
-  launch_pdl(k_csr<VS, U, Epi>, spmv_grid((int64_t)n * VS), 256, 0, n, rows, a.rp.p, a.ci.p, a.v.p, x, epi)
-    switch (c) {
-      case 0: LAUNCH(1, 2); break;
-      case 1: LAUNCH(2, 3); break;
-      case 2: LAUNCH(4, 3); break;
-      case 3: LAUNCH(8, 3); break;
-      case 4: LAUNCH(16, 3); break;
-      case 5: LAUNCH(32, 3); break;
-      default: LAUNCH(32, 4); break;
-    }
-#undef LAUNCH
-    check_launch("csr spmv");
-  };
-  if (!pl.binned) {
-    // lane-group size from the average row length (measured better than
-    // per-class binning: the row-list indirection adds a dependent load)
-    if (avg <= 2.5) LAUNCH_AVG(2, 2);
-    else if (avg <= 5) LAUNCH_AVG(4, 2);
-    else if (avg <= 9) LAUNCH_AVG(4, 3);
-    else if (avg <= 18) LAUNCH_AVG(8, 3);
-    // measured on the config-3 hierarchies (tools/kbench.py): 8 lanes x 2 for
-    // ~26/row (F-relax A_1, 58 -> 68% of HBM), 8 x 4 for ~40-60/row, 16 x 4
-    // for the ~100-150/row coarse-AMG levels (76 -> 84%)
-    else if (avg <= 36) LAUNCH_AVG(8, 2);
-    else if (avg <= 72) LAUNCH_AVG(8, 4);
-    else LAUNCH_AVG(16, 4);
-    check_launch("csr spmv");
-    return;
-  }
-  for (int c = 0; c < SpmvPlan::NC; ++c) run(c, pl.cnt[c], pl.rows.p + pl.off[c]);
+  // lane-group size from the average row length (measured better than per-class
+  // row binning: the row-list indirection adds a dependent load)
+  if (avg <= 2.5) LAUNCH_AVG(2, 2);
+  else if (avg <= 5) LAUNCH_AVG(4, 2);
+  else if (avg <= 9) LAUNCH_AVG(4, 3);
+  else if (avg <= 18) LAUNCH_AVG(8, 3);
+  // measured on the config-3 hierarchies (tools/kbench.py): 8 lanes x 2 for
+  // ~26/row (F-relax A_1, 58 -> 68% of HBM), 8 x 4 for ~40-60/row, 16 x 4
+  // for the ~100-150/row coarse-AMG levels (76 -> 84%)
+  else if (avg <= 36) LAUNCH_AVG(8, 2);
+  else if (avg <= 72) LAUNCH_AVG(8, 4);
+  else LAUNCH_AVG(16, 4);
+#undef LAUNCH_AVG
+  check_launch("csr spmv");
 }
 
 static bool bsell_enabled() {
@@ -494,7 +426,7 @@ static bool bsell_enabled() {
 
 void spmv(const Csr &a, const double *x, double *y) {
   if (a.b == 1) {
-    launch_csr(a, x, EpiStore{y});
+    launch_csr(a, XPlain{x}, EpiStore{y});
     return;
   }
   if (a.nr == 0) return;
@@ -524,21 +456,21 @@ void spmv(const Csr &a, const double *x, double *y) {
 
 void residual(const Csr &a, const double *x, const double *b, double *r) {
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "residual: scalar CSR only");
-  launch_csr(a, x, EpiResid{b, r});
+  launch_csr(a, XPlain{x}, EpiResid{b, r});
 }
 
 void spmv_merge_add(const Csr &a, const double *x, const int *fmap, const double *ef, double *y) {
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spmv_merge_add: scalar CSR only");
-  launch_csr(a, x, EpiMergeAdd{fmap, ef, y});
+  launch_csr(a, XPlain{x}, EpiMergeAdd{fmap, ef, y});
 }
 
 void spmv_add(const Csr &a, const double *x, double *y) {
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spmv_add: scalar CSR only");
-  launch_csr(a, x, EpiAdd{y});
+  launch_csr(a, XPlain{x}, EpiAdd{y});
 }
 
 void jacobi_sweep(const Csr &a, const double *x, const double *b, const double *dinv, double *xo) {
-  launch_csr(a, x, EpiJacobi{x, b, dinv, xo});
+  launch_csr(a, XPlain{x}, EpiJacobi{x, b, dinv, xo});
 }
 
 }  // namespace mg
