@@ -218,7 +218,10 @@ bool pdl_enabled() {
   return on;
 }
 
+static bool timeline_on();
+
 bool trace_on() {
+  if (timeline_on()) return false;          // timeline mode: no synchronising trace
   if (g_ctx && g_ctx->owner) return false;  // worker threads do not trace
   static int on = -1;
   if (on < 0) {
@@ -228,9 +231,41 @@ bool trace_on() {
   return on;
 }
 
+// MG_TIMELINE=1: non-synchronising host timestamps of the trace points of both
+// setup threads (parent and F-relaxation worker), dumped at the end of a setup
+static std::mutex tl_mu;
+static std::vector<std::pair<double, std::string>> tl_events;
+static std::chrono::steady_clock::time_point tl_t0;
+static bool timeline_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_TIMELINE");
+    on = e && *e == '1';
+  }
+  return on;
+}
+void timeline_reset() {
+  if (!timeline_on()) return;
+  std::lock_guard<std::mutex> lk(tl_mu);
+  tl_events.clear();
+  tl_t0 = std::chrono::steady_clock::now();
+}
+void timeline_dump() {
+  if (!timeline_on()) return;
+  std::lock_guard<std::mutex> lk(tl_mu);
+  for (auto &e : tl_events) fprintf(stderr, "[tl] %8.3f ms  %s\n", e.first, e.second.c_str());
+  tl_events.clear();
+}
+
 void trace(const char *what) {
   static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
   static int64_t last_syncs = 0, last_launches = 0;
+  if (timeline_on() && g_ctx) {
+    double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl_t0).count();
+    std::lock_guard<std::mutex> lk(tl_mu);
+    tl_events.emplace_back(t, std::string(g_ctx->owner ? "    [worker] " : "") + what);
+    return;
+  }
   if (!trace_on()) return;
   sync();
   int64_t ds = g_ctx->syncs - last_syncs, dl = g_ctx->launches - last_launches;

@@ -223,6 +223,8 @@ inline int grid_for(int64_t work, int block, int max_blocks = 0) {
 // MG_TRACE=1: synchronise and print the wall time since the previous mark
 void trace(const char *what);
 bool trace_on();
+void timeline_reset();
+void timeline_dump();
 
 // host <-> device helpers (synchronous on the ctx stream)
 void h2d(void *dst, const void *src, size_t bytes);

@@ -114,7 +114,7 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
   while (h->L.back().n > o.cutoff && (int)h->L.size() < o.max_levels) {
     int li = (int)h->L.size() - 1;
     AmgLevel &cur = h->L[li];
-    if (trace_on()) {
+    {
       char msg[96];
       snprintf(msg, sizeof msg, "amg level %d start n=%d nnz=%lld", li, cur.n, (long long)cur.A.nnz);
       trace(msg);
@@ -416,6 +416,7 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "mgr_setup: scalar CSR required");
   if (a.nr != a.nc) throw MgError(MG_ERR_DIM_MISMATCH, "mgr_setup: square matrix required");
   if (coarse_kind != 0 && coarse_kind != 1) throw MgError(MG_ERR_BAD_OPTION, "unknown coarse solver");
+  timeline_reset();
   trace("mgr: enter");
   auto h = std::make_unique<Mgr>();
   h->n0 = a.nr;
@@ -423,7 +424,8 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
   h->coarse_kind = coarse_kind;
   h->L.reserve(plan.size());
   TaskGroup tasks;  // declared after h: joined before h can be destroyed
-  int parent_level = -1;  // MGR level this thread is building (task k = level k)
+  int parent_level = -1;       // MGR level this thread is building
+  std::vector<int> task_level;  // MGR level of each worker task
   try {
     Csr cur = copy_csr(a);
     // per-unknown owning cell, tracked down the levels only when a level relaxes globally
@@ -464,6 +466,7 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
           prepare_spmv(lvp->Aff);
           trace("mgr: F-solver setup");
         });
+        task_level.push_back(parent_level);
       }
       build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
       trace("mgr: build_rp");
@@ -471,13 +474,6 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       trace("mgr: A*P");
       Csr ac = spgemm(lv.R, ap);
       trace("mgr: R*(AP)");
-      if (!post_smoothing && !sp.global_relax) {
-        // after the F-relaxation from e = 0, e is zero on C: r - A e = r - A[:, F] e_F
-        DBuf<int> allrows(n);
-        iota_i32(allrows.p, n);
-        lv.AF = extract(cur, allrows.p, n, fmap.p, lv.nf);
-        prepare_spmv(lv.AF);
-      }
       if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
       if (need_cells) {
         std::vector<int64_t> nxt_cells(lv.nc);
@@ -486,16 +482,32 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
         for (int c = 0; c < lv.nc; ++c) nxt_cells[c] = cells[cl[c]];
         cells.swap(nxt_cells);
       }
-      prepare_spmv(cur);
-      prepare_spmv(lv.R);
-      prepare_spmv(lv.P);
-      lv.res.alloc(n);
-      lv.rF.alloc(lv.nf);
-      lv.eF.alloc(lv.nf);
-      lv.rc.alloc(lv.nc);
-      lv.ec.alloc(lv.nc);
       lv.A = std::move(cur);
       cur = std::move(ac);
+      // the solve-phase preparation of this level (A[:, F], SELL copies, work
+      // vectors) is independent of everything below: a second worker
+      {
+        MgrLevel *lvp = &lv;
+        const bool want_af = !post_smoothing && !sp.global_relax;
+        tasks.run([lvp, want_af, n]() {
+          if (want_af) {
+            // after the F-relaxation from e = 0, e is zero on C: r - A e = r - A[:, F] e_F
+            DBuf<int> allrows(n);
+            iota_i32(allrows.p, n);
+            lvp->AF = extract(lvp->A, allrows.p, n, lvp->fmap.p, lvp->nf);
+            prepare_spmv(lvp->AF);
+          }
+          prepare_spmv(lvp->A);
+          prepare_spmv(lvp->R);
+          prepare_spmv(lvp->P);
+          lvp->res.alloc(n);
+          lvp->rF.alloc(lvp->nf);
+          lvp->eF.alloc(lvp->nf);
+          lvp->rc.alloc(lvp->nc);
+          lvp->ec.alloc(lvp->nc);
+        });
+        task_level.push_back(parent_level);
+      }
     }
     parent_level = 1 << 30;  // below every level
     trace("mgr: levels done");
@@ -519,11 +531,13 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
     // this thread's error, this level's F-solver error loses to it
     std::exception_ptr pe = std::current_exception();
     std::vector<std::exception_ptr> we = tasks.join_errors();
-    for (int k = 0; k < (int)we.size() && k < parent_level; ++k)
-      if (we[k]) std::rethrow_exception(we[k]);
+    for (int k = 0; k < (int)we.size(); ++k)
+      if (we[k] && task_level[k] < parent_level) std::rethrow_exception(we[k]);
     std::rethrow_exception(pe);
   }
   tasks.join();  // F-solver errors of any level
+  trace("mgr: joined");
+  timeline_dump();
   return h;
 }
 
