@@ -140,7 +140,13 @@ void TaskGroup::run(std::function<void()> fn) {
     w->num_sms = p->num_sms;
     w->owner = p;
     w->pool_id = (int)p->workers.size() + 1;
-    MG_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+    // worker streams at the lowest priority: the parent's stream carries the
+    // setup's critical path (MGR RAP, coarse AMG); worker blocks fill the gaps
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char *pe = getenv("MG_WORKER_PRIORITY");
+    int prio = (pe && *pe == '0') ? 0 : lo;
+    MG_CUDA(cudaStreamCreateWithPriority(&w->stream, cudaStreamNonBlocking, prio));
     p->workers.push_back(std::move(w));
   }
   Ctx *w = p->workers[k].get();
