@@ -116,6 +116,44 @@ int mg_ilu_matrix(mg_ctx *ctx, const mg_ilu *f, mg_mat **out);
 int mg_ilu_apply(mg_ctx *ctx, mg_ilu *f, const double *r, double *x);
 int mg_ilu_free(mg_ctx *ctx, mg_ilu *f);
 
+/* ---- Newton system assembly (assembly.py:247-346) -- */
+/* Problem description: the reference Problem's precomputed geometry (interior
+ * faces a -> b with T, T_geo, g.dx; Dirichlet faces with their rule; per-cell
+ * incidence lists in the reference's np.add.at order), constitutive models and
+ * fluid constants.  Host arrays, copied at mg_asm_create. */
+typedef struct {
+  int n_cells, n_faces, n_dirichlet, n_neumann, n_rules;
+  double cell_volume;
+  /* fluid (physics.FluidParams; c_h, c_v precomputed) */
+  double phi, diff_lh, mu_l, mu_g, rho_w_std, c_h, c_v;
+  /* relperm / capillary models (van_genuchten flag, parameters, m = 1 - 1/n) */
+  int rp_van_genuchten;
+  double s_lr, s_gr, rp_m, rp_eps;
+  int cp_van_genuchten;
+  double p_entry, cp_n, cp_m, cp_eps;
+  const int *face_a, *face_b;                      /* n_faces */
+  const double *trans, *tgeo, *gdx;                /* n_faces */
+  const int *dir_cell, *dir_rule;                  /* n_dirichlet */
+  const double *dir_trans, *dir_tgeo, *dir_gdx;    /* n_dirichlet */
+  /* Dirichlet rule ghost states: p_l, s_l, rho_lh, P_c, dP_c, lambda_l, lambda_g */
+  const double *rule_p, *rule_s, *rule_rho, *rule_pc, *rule_dpc, *rule_lam_l, *rule_lam_g;
+  /* per-cell incidence (n_cells + 1 offsets): entries f (a-side interior face),
+   * f + 2^30 (b-side interior face), n_faces + q (Dirichlet face q), -1 - k
+   * (Neumann contribution k); in the reference's accumulation order */
+  const int *inc_rp, *inc_ent;
+  const double *neu_w, *neu_h;                     /* n_neumann: -w*area, -h*area */
+} mg_asm_desc;
+typedef struct mg_asm mg_asm;
+int mg_asm_create(mg_ctx *ctx, const mg_asm_desc *d, mg_asm **out);
+/* Residual (host res[3 n]), active set (host active[n], 1 = gas present) and,
+ * when jac_out != NULL, the Jacobian as a 3n x 3n scalar CSR device matrix
+ * (variable-major, duplicates merged, explicit zeros kept).  States are host
+ * arrays of n: p_l, s_l, rho_lh and the previous step's. */
+int mg_asm_assemble(mg_ctx *ctx, mg_asm *a, const double *p, const double *s, const double *rho,
+                    const double *p_old, const double *s_old, const double *rho_old, double dt, double *res,
+                    int *active, mg_mat **jac_out);
+int mg_asm_free(mg_ctx *ctx, mg_asm *a);
+
 /* ---- MGR build_rp (mgr.py:117-156) ------------------------------------------ */
 enum { MG_RP_INJECTIVE = 0, MG_RP_NONINJECTIVE = 1, MG_RP_INJECTION = 2, MG_RP_IDEAL = 3 };
 int mg_build_rp(mg_ctx *ctx, const mg_mat *a, const uint8_t *f_mask, int kind, mg_mat **r_out,

@@ -93,6 +93,9 @@ _SIGS = {
     "mg_ilu_matrix": [P, P, ctypes.POINTER(P)],
     "mg_ilu_apply": [P, P, P, P],
     "mg_ilu_free": [P, P],
+    "mg_asm_create": [P, P, ctypes.POINTER(P)],
+    "mg_asm_assemble": [P, P, P, P, P, P, P, P, c_double, P, P, ctypes.POINTER(P)],
+    "mg_asm_free": [P, P],
     "mg_dev_alloc": [P, c_int64, ctypes.POINTER(P)],
     "mg_dev_free": [P, P],
     "mg_memcpy_h2d": [P, P, P, c_int64],

@@ -19,6 +19,18 @@ struct mg_amg {
 };
 struct mg_mgr { std::unique_ptr<Mgr> h; };
 struct mg_ilu { std::unique_ptr<Ilu> f; };
+namespace mg {
+struct AsmGeo;
+AsmGeo *asm_create(const mg_asm_desc &d);
+void asm_destroy(AsmGeo *g);
+void asm_assemble(AsmGeo &g, const double *p, const double *s, const double *r, const double *p_old,
+                  const double *s_old, const double *r_old, double dt, double *res, int *active, Csr *jac);
+}  // namespace mg
+struct mg_asm {
+  mg::AsmGeo *g = nullptr;
+  int n = 0;
+  ~mg_asm() { if (g) mg::asm_destroy(g); }
+};
 
 namespace {
 struct Enter {
@@ -559,6 +571,37 @@ int mg_ilu_apply(mg_ctx *ctx, mg_ilu *f, const double *r, double *x) {
 
 int mg_ilu_free(mg_ctx *ctx, mg_ilu *f) {
   return guard(ctx, [&] { delete f; });
+}
+
+int mg_asm_create(mg_ctx *ctx, const mg_asm_desc *d, mg_asm **out) {
+  return guard(ctx, [&] {
+    if (!d || d->n_cells <= 0) throw MgError(MG_ERR_BAD_OPTION, "assembly: empty problem");
+    auto h = std::make_unique<mg_asm>();
+    h->g = asm_create(*d);
+    h->n = d->n_cells;
+    *out = h.release();
+  });
+}
+
+int mg_asm_assemble(mg_ctx *ctx, mg_asm *a, const double *p, const double *s, const double *rho,
+                    const double *p_old, const double *s_old, const double *rho_old, double dt, double *res,
+                    int *active, mg_mat **jac_out) {
+  return guard(ctx, [&] {
+    const int n = a->n;
+    DevVec dp(p, n), ds(s, n), dr(rho, n), dpo(p_old, n), dso(s_old, n), dro(rho_old, n), dres(nullptr, 3 * (int64_t)n);
+    DBuf<int> dact(n);
+    std::unique_ptr<mg_mat> m;
+    if (jac_out) m = std::make_unique<mg_mat>();
+    asm_assemble(*a->g, dp.b.p, ds.b.p, dr.b.p, dpo.b.p, dso.b.p, dro.b.p, dt, dres.b.p, dact.p,
+                 m ? &m->m : nullptr);
+    if (res) d2h(res, dres.b.p, sizeof(double) * 3 * (size_t)n);
+    if (active) d2h(active, dact.p, sizeof(int) * (size_t)n);
+    if (jac_out) *jac_out = m.release();
+  });
+}
+
+int mg_asm_free(mg_ctx *ctx, mg_asm *a) {
+  return guard(ctx, [&] { delete a; });
 }
 
 int mg_dev_alloc(mg_ctx *ctx, int64_t bytes, void **out) {
