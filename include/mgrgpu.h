@@ -59,6 +59,17 @@ int mg_mat_upload_csr(mg_ctx *ctx, int nrows, int ncols, const int32_t *indptr,
 /* block CSR: nbrows block rows, b x b row-major blocks, sorted block columns */
 int mg_mat_upload_bsr(mg_ctx *ctx, int nbrows, int nbcols, int b, const int32_t *rowptr,
                       const int32_t *colind, const double *vals, mg_mat **out);
+/* mg_mat_upload_bsr without the host wait: the copies run on the context's
+   copy stream and overlap whatever the context is computing; the first call
+   that uses the matrix (or mg_mat_free) orders the context stream after them.
+   The host arrays must stay valid and unmodified until the context has
+   synchronised after that first use (any call returning a host result, or
+   mg_ctx_sync) or mg_mat_free has returned, and must be
+   pinned for the copies to be asynchronous (pageable memory still works, the
+   driver then stages it synchronously).  Lets a caller upload time step k+1's
+   Jacobian while step k is being solved. */
+int mg_mat_upload_bsr_async(mg_ctx *ctx, int nbrows, int nbcols, int b, const int32_t *rowptr,
+                            const int32_t *colind, const double *vals, mg_mat **out);
 /* nrows/ncols are scalar dims for CSR and block dims for BSR */
 int mg_mat_info(mg_ctx *ctx, const mg_mat *m, int *nrows, int *ncols, int64_t *nnz, int *b);
 int mg_mat_download(mg_ctx *ctx, const mg_mat *m, int32_t *indptr, int32_t *indices,

@@ -11,7 +11,19 @@
 using namespace mg;
 
 struct mg_ctx { Ctx c; };
-struct mg_mat { Csr m; };
+// `ready` is set while an asynchronous upload (mg_mat_upload_bsr_async) may
+// still be in flight on the context's copy stream: the first use of the
+// matrix orders the context stream after it (C() below).
+struct mg_mat {
+  Csr m;
+  cudaEvent_t ready = nullptr;
+  ~mg_mat() {
+    if (ready) {  // never used: the copies land before the buffers (and the host arrays) are released
+      cudaEventSynchronize(ready);
+      cudaEventDestroy(ready);
+    }
+  }
+};
 struct mg_amg {
   Amg *h = nullptr;
   bool owned = true;
@@ -59,6 +71,17 @@ int guard(mg_ctx *ctx, F &&f) {
     ctx->c.err = ex.what();
     return MG_ERR_CUDA;
   }
+}
+
+// input matrix of an API call: waits for a pending asynchronous upload
+Csr &C(const mg_mat *x) {
+  auto *m = const_cast<mg_mat *>(x);
+  if (m->ready) {
+    MG_CUDA(cudaStreamWaitEvent(stream(), m->ready, 0));
+    cudaEventDestroy(m->ready);
+    m->ready = nullptr;
+  }
+  return m->m;
 }
 
 Csr upload_csr(int nrows, int ncols, int b, const int32_t *indptr, const int32_t *indices, const double *vals) {
@@ -134,6 +157,10 @@ int mg_ctx_destroy(mg_ctx *ctx) {
     Enter e(ctx);
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.hbuf) cudaFreeHost(ctx->c.hbuf);
+    if (ctx->c.copy_stream) {
+      cudaStreamSynchronize(ctx->c.copy_stream);
+      cudaStreamDestroy(ctx->c.copy_stream);
+    }
     alloc_release_cache(&ctx->c);
     for (auto &kv : ctx->c.block_size) cudaFree(kv.first);  // blocks still owned by live handles
     ctx->c.block_size.clear();
@@ -169,18 +196,48 @@ int mg_mat_upload_bsr(mg_ctx *ctx, int nbrows, int nbcols, int b, const int32_t 
   });
 }
 
+int mg_mat_upload_bsr_async(mg_ctx *ctx, int nbrows, int nbcols, int b, const int32_t *rowptr,
+                            const int32_t *colind, const double *vals, mg_mat **out) {
+  return guard(ctx, [&] {
+    if (b < 1 || b > 3) throw MgError(MG_ERR_UNSUPPORTED, "block size must be 1, 2 or 3");
+    if (nbrows < 0 || nbcols < 0) throw MgError(MG_ERR_BAD_OPTION, "negative dimension");
+    if (rowptr[0] != 0) throw MgError(MG_ERR_BAD_OPTION, "indptr must start at 0");
+    int64_t nnz = rowptr[nbrows];
+    Ctx &c = *g_ctx;
+    if (!c.copy_stream) MG_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    auto *m = new mg_mat();
+    try {
+      m->m.alloc(nbrows, nbcols, nnz, b);
+      // pool blocks may have been freed by work still queued on the context stream
+      cudaEvent_t fork;
+      MG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      MG_CUDA(cudaEventRecord(fork, c.stream));
+      MG_CUDA(cudaStreamWaitEvent(c.copy_stream, fork, 0));
+      cudaEventDestroy(fork);
+      MG_CUDA(cudaMemcpyAsync(m->m.rp.p, rowptr, sizeof(int) * ((size_t)nbrows + 1), cudaMemcpyHostToDevice,
+                              c.copy_stream));
+      MG_CUDA(cudaMemcpyAsync(m->m.ci.p, colind, sizeof(int) * (size_t)nnz, cudaMemcpyHostToDevice, c.copy_stream));
+      MG_CUDA(cudaMemcpyAsync(m->m.v.p, vals, sizeof(double) * (size_t)nnz * b * b, cudaMemcpyHostToDevice,
+                              c.copy_stream));
+      MG_CUDA(cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming));
+      MG_CUDA(cudaEventRecord(m->ready, c.copy_stream));
+    } catch (...) { delete m; throw; }
+    *out = m;
+  });
+}
+
 int mg_mat_info(mg_ctx *ctx, const mg_mat *m, int *nrows, int *ncols, int64_t *nnz, int *b) {
   return guard(ctx, [&] {
-    if (nrows) *nrows = m->m.nr;
-    if (ncols) *ncols = m->m.nc;
-    if (nnz) *nnz = m->m.nnz;
-    if (b) *b = m->m.b;
+    if (nrows) *nrows = C(m).nr;
+    if (ncols) *ncols = C(m).nc;
+    if (nnz) *nnz = C(m).nnz;
+    if (b) *b = C(m).b;
   });
 }
 
 int mg_mat_download(mg_ctx *ctx, const mg_mat *m, int32_t *indptr, int32_t *indices, double *vals) {
   return guard(ctx, [&] {
-    const Csr &c = m->m;
+    const Csr &c = C(m);
     if (indptr) d2h(indptr, c.rp.p, sizeof(int) * ((size_t)c.nr + 1));
     if (indices) d2h(indices, c.ci.p, sizeof(int) * (size_t)c.nnz);
     if (vals) d2h(vals, c.v.p, sizeof(double) * (size_t)c.nnz * c.b * c.b);
@@ -193,7 +250,7 @@ int mg_mat_free(mg_ctx *ctx, mg_mat *m) {
 
 int mg_spmv(mg_ctx *ctx, const mg_mat *a, const double *x, double *y) {
   return guard(ctx, [&] {
-    const Csr &c = a->m;
+    const Csr &c = C(a);
     DevVec dx(x, (int64_t)c.nc * c.b), dy(nullptr, vec_len(c));
     spmv(c, dx.b.p, dy.b.p);
     d2h(y, dy.b.p, sizeof(double) * vec_len(c));
@@ -201,24 +258,24 @@ int mg_spmv(mg_ctx *ctx, const mg_mat *a, const double *x, double *y) {
 }
 
 int mg_spmv_dev(mg_ctx *ctx, const mg_mat *a, const double *x_dev, double *y_dev) {
-  return guard(ctx, [&] { spmv(a->m, x_dev, y_dev); });
+  return guard(ctx, [&] { spmv(C(a), x_dev, y_dev); });
 }
 
 int mg_matmul(mg_ctx *ctx, const mg_mat *a, const mg_mat *b, mg_mat **out) {
   return guard(ctx, [&] {
     auto *m = new mg_mat();
-    try { m->m = spgemm(a->m, b->m); } catch (...) { delete m; throw; }
+    try { m->m = spgemm(C(a), C(b)); } catch (...) { delete m; throw; }
     *out = m;
   });
 }
 
 int mg_triple_product(mg_ctx *ctx, const mg_mat *r, const mg_mat *a, const mg_mat *p, mg_mat **out) {
   return guard(ctx, [&] {
-    if (r->m.nc != a->m.nr || a->m.nc != p->m.nr)
+    if (C(r).nc != C(a).nr || C(a).nc != C(p).nr)
       throw MgError(MG_ERR_DIM_MISMATCH, "triple_product: inner dimensions differ");
-    Csr ap = spgemm(a->m, p->m);
+    Csr ap = spgemm(C(a), C(p));
     auto *m = new mg_mat();
-    try { m->m = spgemm(r->m, ap); } catch (...) { delete m; throw; }
+    try { m->m = spgemm(C(r), ap); } catch (...) { delete m; throw; }
     *out = m;
   });
 }
@@ -226,7 +283,7 @@ int mg_triple_product(mg_ctx *ctx, const mg_mat *r, const mg_mat *a, const mg_ma
 int mg_transpose(mg_ctx *ctx, const mg_mat *a, mg_mat **out) {
   return guard(ctx, [&] {
     auto *m = new mg_mat();
-    try { m->m = transpose(a->m); } catch (...) { delete m; throw; }
+    try { m->m = transpose(C(a)); } catch (...) { delete m; throw; }
     *out = m;
   });
 }
@@ -234,7 +291,7 @@ int mg_transpose(mg_ctx *ctx, const mg_mat *a, mg_mat **out) {
 int mg_extract(mg_ctx *ctx, const mg_mat *a, const int64_t *rows, int nr, const int64_t *cols, int nc,
                mg_mat **out) {
   return guard(ctx, [&] {
-    const Csr &c = a->m;
+    const Csr &c = C(a);
     if (c.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "extract: scalar CSR only");
     std::vector<int> hr(nr), cmap(c.nc, -1);
     for (int i = 0; i < nr; ++i) {
@@ -260,7 +317,7 @@ int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, int equilibrate, mg_mat **d
   return guard(ctx, [&] {
     auto d = std::make_unique<mg_mat>();
     auto ah = std::make_unique<mg_mat>();
-    block_scale(a_bsr->m, d->m, ah->m, equilibrate != 0);
+    block_scale(C(a_bsr), d->m, ah->m, equilibrate != 0);
     *dinv_out = d.release();
     *ahat_out = ah.release();
   });
@@ -268,11 +325,11 @@ int mg_block_scale(mg_ctx *ctx, const mg_mat *a_bsr, int equilibrate, mg_mat **d
 
 int mg_equilibrate(mg_ctx *ctx, const mg_mat *a, mg_mat **scaled_out, double *row_out, double *col_scale_out) {
   return guard(ctx, [&] {
-    if (a->m.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "equilibrate: scalar CSR required");
-    int n = a->m.nr;
+    if (C(a).b != 1) throw MgError(MG_ERR_UNSUPPORTED, "equilibrate: scalar CSR required");
+    int n = C(a).nr;
     DBuf<double> row((size_t)(n ? n : 1)), cs((size_t)(n ? n : 1));
     auto o = std::make_unique<mg_mat>();
-    equilibrate(a->m, o->m, row.p, cs.p);
+    equilibrate(C(a), o->m, row.p, cs.p);
     if (row_out) d2h(row_out, row.p, sizeof(double) * n);
     if (col_scale_out) d2h(col_scale_out, cs.p, sizeof(double) * n);
     *scaled_out = o.release();
@@ -280,21 +337,21 @@ int mg_equilibrate(mg_ctx *ctx, const mg_mat *a, mg_mat **scaled_out, double *ro
 }
 
 int mg_abs_row_sum_max(mg_ctx *ctx, const mg_mat *a, double *out) {
-  return guard(ctx, [&] { *out = abs_row_sum_max(a->m); });
+  return guard(ctx, [&] { *out = abs_row_sum_max(C(a)); });
 }
 
 int mg_block_apply(mg_ctx *ctx, const mg_mat *dinv, const double *v, double *z) {
   return guard(ctx, [&] {
-    int64_t n = vec_len(dinv->m);
+    int64_t n = vec_len(C(dinv));
     DevVec dv(v, n), dz(nullptr, n);
-    block_apply(dinv->m, dv.b.p, dz.b.p);
+    block_apply(C(dinv), dv.b.p, dz.b.p);
     d2h(z, dz.b.p, sizeof(double) * n);
   });
 }
 
 int mg_build_rp(mg_ctx *ctx, const mg_mat *a, const uint8_t *f_mask, int kind, mg_mat **r_out, mg_mat **p_out) {
   return guard(ctx, [&] {
-    const Csr &c = a->m;
+    const Csr &c = C(a);
     if (c.b != 1 || c.nr != c.nc) throw MgError(MG_ERR_DIM_MISMATCH, "build_rp: square scalar CSR required");
     if (kind < 0 || kind > 3) throw MgError(MG_ERR_BAD_OPTION, "unknown RpKind");
     int n = c.nr;
@@ -314,7 +371,7 @@ int mg_build_rp(mg_ctx *ctx, const mg_mat *a, const uint8_t *f_mask, int kind, m
 int mg_amg_setup(mg_ctx *ctx, const mg_mat *a, const mg_amg_opts *opts, mg_amg **out) {
   return guard(ctx, [&] {
     auto h = std::make_unique<mg_amg>();
-    h->h = amg_setup(a->m, conv(opts)).release();
+    h->h = amg_setup(C(a), conv(opts)).release();
     *out = h.release();
   });
 }
@@ -380,7 +437,7 @@ int mg_amg_free(mg_ctx *ctx, mg_amg *h) {
 int mg_mgr_setup(mg_ctx *ctx, const mg_mat *a, const mg_level_spec *plan, int nlevels, const mg_amg_opts *amg_opts,
                  int coarse_kind, int post_smoothing, const int64_t *cells, mg_mgr **out) {
   return guard(ctx, [&] {
-    const Csr &c = a->m;
+    const Csr &c = C(a);
     std::vector<LevelSpec> specs;
     int n = c.nr;
     for (int k = 0; k < nlevels; ++k) {
@@ -421,8 +478,8 @@ int mg_mgr_setup(mg_ctx *ctx, const mg_mat *a, const mg_level_spec *plan, int nl
 
 int mg_mgr_set_prescale(mg_ctx *ctx, mg_mgr *h, const mg_mat *dinv) {
   return guard(ctx, [&] {
-    if (vec_len(dinv->m) != h->h->n0) throw MgError(MG_ERR_DIM_MISMATCH, "prescale dimension mismatch");
-    h->h->prescale = copy_csr(dinv->m);
+    if (vec_len(C(dinv)) != h->h->n0) throw MgError(MG_ERR_DIM_MISMATCH, "prescale dimension mismatch");
+    h->h->prescale = copy_csr(C(dinv));
     h->h->has_prescale = true;
     h->h->drop_graph();
     h->h->pre_buf.alloc((size_t)h->h->n0);
@@ -500,7 +557,7 @@ static int gmres_common(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b
   cudaEventCreate(&e1);
   prof_reset();
   cudaEventRecord(e0, stream());
-  GmresOut out = gmres(a->m, m ? m->h.get() : nullptr, b_dev, x_dev, o, a_norm, ilu);
+  GmresOut out = gmres(C(a), m ? m->h.get() : nullptr, b_dev, x_dev, o, a_norm, ilu);
   cudaEventRecord(e1, stream());
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -509,7 +566,7 @@ static int gmres_common(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b
   cudaEventDestroy(e1);
   prof_collect();
   g_ctx->timing.solve_ms = ms;
-  g_ctx->timing.spmv_bytes = a->m.bytes_spmv();
+  g_ctx->timing.spmv_bytes = C(a).bytes_spmv();
   g_ctx->timing.vcycle_bytes = (m && m->h->camg) ? m->h->camg->cycle_bytes() : 0.0;
   g_ctx->timing.k0_bytes = (m && m->h->camg) ? m->h->camg->k0_bytes() : 0.0;
   res->iterations = out.iterations;
@@ -522,7 +579,7 @@ static int gmres_common(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b
 int mg_gmres(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b, double *x, const mg_gmres_opts *opts,
              double a_norm, mg_gmres_result *res) {
   return guard(ctx, [&] {
-    int64_t n = vec_len(a->m);
+    int64_t n = vec_len(C(a));
     DevVec db(b, n), dx(nullptr, n);
     gmres_common(ctx, a, m, db.b.p, dx.b.p, opts, a_norm, res);
     d2h(x, dx.b.p, sizeof(double) * n);
@@ -537,7 +594,7 @@ int mg_gmres_dev(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b_dev, d
 int mg_gmres_ilu(mg_ctx *ctx, const mg_mat *a, mg_ilu *f, const double *b, double *x, const mg_gmres_opts *opts,
                  double a_norm, mg_gmres_result *out) {
   return guard(ctx, [&] {
-    int64_t n = vec_len(a->m);
+    int64_t n = vec_len(C(a));
     DevVec db(b, n), dx(nullptr, n);
     gmres_common(ctx, a, nullptr, db.b.p, dx.b.p, opts, a_norm, out, f ? f->f.get() : nullptr);
     d2h(x, dx.b.p, sizeof(double) * n);
@@ -547,7 +604,7 @@ int mg_gmres_ilu(mg_ctx *ctx, const mg_mat *a, mg_ilu *f, const double *b, doubl
 int mg_ilu_factor(mg_ctx *ctx, const mg_mat *a, int level, mg_ilu **out) {
   return guard(ctx, [&] {
     auto h = std::make_unique<mg_ilu>();
-    h->f = ilu_factor(a->m, level);
+    h->f = ilu_factor(C(a), level);
     *out = h.release();
   });
 }

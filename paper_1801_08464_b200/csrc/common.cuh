@@ -55,6 +55,7 @@ struct Ctx {
   void *cub_tmp = nullptr;
   size_t cub_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // mg_timer_start / mg_timer_stop
+  cudaStream_t copy_stream = nullptr;         // mg_mat_upload_bsr_async (created on first use)
   // caching allocator state (common.cu); owned by the API context, shared by
   // its worker contexts under `amu`.  Every block has a home pool (the context
   // that cudaMalloc'ed it: 0 = API context, k = worker k) and returns there

@@ -19,12 +19,13 @@ from .errors import DimensionMismatch
 class DeviceMatrix:
     """Scalar CSR (b=1) or block CSR (b=2,3) matrix resident in HBM."""
 
-    __slots__ = ("ctx", "h", "_info")
+    __slots__ = ("ctx", "h", "_info", "_keep")
 
-    def __init__(self, ctx, handle):
+    def __init__(self, ctx, handle, keep=None):
         self.ctx = ctx
         self.h = handle
         self._info = None
+        self._keep = keep  # host arrays an asynchronous upload may still be reading
 
     # -- construction -----------------------------------------------------
     @classmethod
@@ -37,16 +38,22 @@ class DeviceMatrix:
         return cls(ctx, h)
 
     @classmethod
-    def from_bsr(cls, rowptr, colind, blocks, nbcols=None, ctx=None):
+    def from_bsr(cls, rowptr, colind, blocks, nbcols=None, ctx=None, asynchronous=False):
+        """Upload a block CSR matrix.  ``asynchronous=True`` returns at once and
+        copies on the context's copy stream (mg_mat_upload_bsr_async), so the
+        next system can be uploaded while the current one is solved; the
+        arrays must then be pinned to overlap, and are kept referenced by the
+        returned matrix."""
         ctx = ctx or _lib.ctx()
         blocks = _lib.f64(blocks)
         b = blocks.shape[-1]
         rp, ci = _lib.i32(rowptr), _lib.i32(colind)
         nb = rp.size - 1
         h = _lib.P()
-        ctx.call("mg_mat_upload_bsr", nb, int(nbcols if nbcols is not None else nb), int(b), _lib.ptr(rp),
+        fn = "mg_mat_upload_bsr_async" if asynchronous else "mg_mat_upload_bsr"
+        ctx.call(fn, nb, int(nbcols if nbcols is not None else nb), int(b), _lib.ptr(rp),
                  _lib.ptr(ci), _lib.ptr(blocks), _lib.ctypes.byref(h))
-        return cls(ctx, h)
+        return cls(ctx, h, (rp, ci, blocks) if asynchronous else None)
 
     @classmethod
     def from_host(cls, a, ctx=None):
@@ -135,6 +142,9 @@ class DeviceMatrix:
         if self.h:
             self.ctx.lib.mg_mat_free(self.ctx.h, self.h)
             self.h = None
+            if self._keep is not None:  # copies of an asynchronous upload have landed before the arrays go
+                self.ctx.sync()
+                self._keep = None
 
     def __del__(self):
         try:

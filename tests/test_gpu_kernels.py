@@ -49,6 +49,29 @@ def test_bsr_spmv_matches_scipy(gpu, cfg, edge):
     assert relerr(gsp.spmv(d, x), a @ x) <= 1e-14
 
 
+def test_async_upload_pipeline(gpu):
+    """mg_mat_upload_bsr_async: matrices uploaded on the copy stream while the
+    context is busy equal synchronous uploads; an async upload freed before
+    any use (the destructor waits for its copies) leaves the pool consistent."""
+    import torch
+    s = synth.make_config(3, 20)
+    rp = torch.from_numpy(np.ascontiguousarray(s.rowptr, dtype=np.int32)).pin_memory().numpy()
+    ci = torch.from_numpy(np.ascontiguousarray(s.col, dtype=np.int32)).pin_memory().numpy()
+    vals = torch.from_numpy(np.ascontiguousarray(s.vals)).pin_memory().numpy()
+    x = np.random.default_rng(5).standard_normal(s.n)
+    ref = gsp.spmv(gsp.DeviceMatrix.from_bsr(s.rowptr, s.col, s.vals), x)
+    unused = gsp.DeviceMatrix.from_bsr(rp, ci, vals, asynchronous=True)
+    unused.free()
+    nxt = gsp.DeviceMatrix.from_bsr(rp, ci, vals, asynchronous=True)
+    for _ in range(3):
+        cur, nxt = nxt, gsp.DeviceMatrix.from_bsr(rp, ci, vals, asynchronous=True)
+        np.testing.assert_array_equal(gsp.spmv(cur, x), ref)
+        ip, ix, v = cur.download()
+        np.testing.assert_array_equal(ix, s.col)
+        cur.free()
+    nxt.free()
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_spgemm_bitwise_scipy(gpu, seed):
     """csr_matmat order, separate mul/add, exact zeros dropped."""
