@@ -16,6 +16,7 @@ rank solves its own system, time = max over ranks, scaling "weak".
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -70,6 +71,14 @@ class ClockSampler:
         except Exception:  # noqa: BLE001
             self.proc = None
 
+    def wait_ready(self, timeout=15.0):
+        """Block until nvidia-smi has produced its first sample: its start-up
+        stalls the driver (tens of ms), which must not land in a timed step."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+        time.sleep(0.2)
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
@@ -102,6 +111,82 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+class NvmlClockSampler:
+    """In-process NVML sampling of the same fields (SM clock, max SM clock,
+    clock-event reasons) every 200 ms during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def __init__(self, device):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        self.rows = []
+        self.i0 = 0
+        self.stop_ev = threading.Event()
+        self.t = None
+
+    def start(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, mx, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            self.stop_ev.wait(0.2)
+
+    def wait_ready(self, timeout=15.0):
+        t0 = time.perf_counter()
+        while not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self):
+        self.i0 = len(self.rows)
+
+    def stop(self):
+        self.stop_ev.set()
+        self.t.join(timeout=2)
+        rows = list(self.rows[self.i0:]) or list(self.rows)
+        reasons = sorted({nm for _, _, r in rows for bit, nm in self.REASONS.items() if r & bit})
+        sm = [float(r[0]) for r in rows]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][1]) if rows else None,
+                "reasons": reasons, "samples": len(sm), "source": "nvml"}
+
+
+class _NoClocks:
+    def start(self):
+        pass
+
+    def wait_ready(self):
+        pass
+
+    def mark(self):
+        pass
+
+    def stop(self):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled (BENCH_CLOCKS=off)"]}
+
+
+def clock_sampler(device):
+    kind = os.environ.get("BENCH_CLOCKS", "smi")
+    if kind == "off":
+        return _NoClocks()
+    if kind == "nvml":
+        try:
+            return NvmlClockSampler(device)
+        except Exception:  # noqa: BLE001
+            pass
+    return ClockSampler(device)
 
 
 def peaks():
@@ -225,21 +310,29 @@ def main():
     gopts = solver.gopts.to_c()
     res = _lib.GmresRes()
 
+    walls = [0.0, 0.0]
+
     def device_step():
+        t0 = time.perf_counter()
         solver.setup()
+        t1 = time.perf_counter()
         ctx.call("mg_gmres_dev", a.h, solver.hier.h, b_dev, x_dev, _lib.ctypes.byref(gopts), -1.0,
                  _lib.ctypes.byref(res))
+        walls[0], walls[1] = 1e3 * (t1 - t0), 1e3 * (time.perf_counter() - t1)
 
     def barrier():
         ctx.sync()
         rep.barrier()
 
-    clk = ClockSampler(local)
+    clk = clock_sampler(local)
     clk.start()  # before the warm-up: nvidia-smi's start-up stalls the driver briefly
+    clk.wait_ready()
     for _ in range(args.warmup):
         device_step()
     barrier()
     # ---- timed region (device-resident inputs) --------------------------------------
+    gc.collect()
+    gc.disable()  # a collector pass (tens of ms with torch loaded) must not land in a timed step
     clk.mark()
     launches0 = ctx.launches
     its = []
@@ -254,7 +347,8 @@ def main():
         t = ctx.timing()
         if dbg:
             ctx.sync()
-            print(f"step wall {1e3 * (time.perf_counter() - tw):.1f} ms setup {t.setup_ms:.1f} solve {t.solve_ms:.1f} "
+            print(f"step wall {1e3 * (time.perf_counter() - tw):.1f} ms (setup call {walls[0]:.1f}, gmres call "
+                  f"{walls[1]:.1f}) setup {t.setup_ms:.1f} solve {t.solve_ms:.1f} "
                   f"dev_bytes {ctx.device_bytes / 2**30:.2f} GiB", file=sys.stderr, flush=True)
         setup_ms.append(t.setup_ms)
         solve_ms.append(t.solve_ms)
@@ -262,6 +356,7 @@ def main():
         conv &= bool(res.converged)
     ev.record_stop()
     barrier()
+    gc.enable()
     total_ms = ev.elapsed_ms()
     clocks = clk.stop()
     launches = ctx.launches - launches0
@@ -371,24 +466,41 @@ def _e2e(ctx, sysm, args, rep, barrier):
     def upload():
         return DeviceMatrix.from_bsr(rp, ci, vals, ctx=ctx, asynchronous=PIPELINE)
 
+    dbg = os.environ.get("BENCH_DEBUG") == "1"
+
     def step(prefetch):
+        t0 = time.perf_counter()
         a = pending[0] if pending[0] is not None else upload()
         pending[0] = upload() if prefetch else None
         solver.a = a
+        t1 = time.perf_counter()
         solver.setup(a, sysm.b, sysm.n_cells)
+        t2 = time.perf_counter()
         ctx.call("mg_gmres", a.h, solver.hier.h, _lib.ptr(rhs), _lib.ptr(xh), _lib.ctypes.byref(gopts), -1.0,
                  _lib.ctypes.byref(res))
+        t3 = time.perf_counter()
         a.free()
+        if dbg:
+            t4 = time.perf_counter()
+            print(f"  upload {1e3 * (t1 - t0):.1f} setup {1e3 * (t2 - t1):.1f} gmres {1e3 * (t3 - t2):.1f} "
+                  f"free {1e3 * (t4 - t3):.1f} ms", file=sys.stderr, flush=True)
 
-    for _ in range(max(1, args.warmup)):
-        step(False)
+    nw = max(1, args.warmup)
+    for i in range(nw):  # the pool settles with two matrices alive; nothing pending afterwards
+        step(PIPELINE and i + 1 < nw)
     barrier()
+    gc.collect()
+    gc.disable()
     ev = _Events(ctx)  # device events on the library stream (host copies run on it too)
     ev.record_start()
     for i in range(args.steps):
+        tw = time.perf_counter()
         step(PIPELINE and i + 1 < args.steps)
+        if dbg:
+            print(f"e2e step wall {1e3 * (time.perf_counter() - tw):.1f} ms", file=sys.stderr, flush=True)
     ev.record_stop()
     barrier()
+    gc.enable()
     el = rep.max(ev.elapsed_ms())
     ms = el / args.steps
     h2d = rp.nbytes + ci.nbytes + vals.nbytes + rhs.nbytes

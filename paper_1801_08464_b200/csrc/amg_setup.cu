@@ -19,25 +19,26 @@ namespace mg {
 enum { UNDEC = 0, FPT = 1, CPT = 2 };
 
 // ---- diagonal ----------------------------------------------------------------
+template <int VS>
 __global__ void k_row_diag(int n, const int *rp, const int *ci, const double *v, double *d) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= n) return;
-  int found = -1;
-  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32)
-    if (ci[q] == wid) found = q;
-  unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
-  double val = 0.0;
-  if (bal) {
-    int src = __ffs(bal) - 1;
-    int q = __shfl_sync(0xffffffffu, found, src);
-    val = __dadd_rn(0.0, v[q]);
+  for (RowGroup<VS> g; g.row < n; g.next()) {
+    const int r = (int)g.row;
+    int found = -1;
+    for (int q = rp[r] + g.lane; q < rp[r + 1]; q += VS)
+      if (ci[q] == r) found = q;
+    unsigned bal = g.ballot(found >= 0);
+    double val = 0.0;
+    if (bal) {
+      int q = g.bcast(found, __ffs(bal) - 1);
+      val = __dadd_rn(0.0, v[q]);
+    }
+    if (g.lane == 0) d[r] = val;
   }
-  if (lane == 0) d[wid] = val;
 }
 
 void row_diag(const Csr &a, double *d) {
   if (!a.nr) return;
-  k_row_diag<<<grid_for((int64_t)a.nr * 32, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, d);
+  MG_ROWGROUP_LAUNCH(k_row_diag, a.nr, a.nnz, a.nr, a.rp.p, a.ci.p, a.v.p, d);
   check_launch("row_diag");
 }
 
@@ -110,36 +111,38 @@ bool sign_normalise(const Csr &a, Csr &out, DBuf<double> &sgn) {
 }
 
 // ---- strength of connection (amg.py:88-103) ------------------------------------
+template <int VS>
 __global__ void k_strength(int n, const int *rp, const int *ci, const double *v, double theta, int8_t *s,
                            int *any) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= n) return;
-  int b = rp[wid], e = rp[wid + 1];
-  bool neg = false;
-  for (int q = b + lane; q < e; q += 32) neg |= (ci[q] != wid) && (v[q] < 0.0);
-  bool has_neg = __any_sync(0xffffffffu, neg);
-  double rmax = 0.0;
-  for (int q = b + lane; q < e; q += 32) {
-    bool off = ci[q] != wid;
-    double a = v[q];
-    double cand = (off && a < 0.0) ? -a : ((off && !has_neg) ? fabs(a) : 0.0);
-    rmax = fmax(rmax, cand);
+  for (RowGroup<VS> g; g.row < n; g.next()) {
+    const int r = (int)g.row;
+    int b = rp[r], e = rp[r + 1];
+    bool neg = false;
+    for (int q = b + g.lane; q < e; q += VS) neg |= (ci[q] != r) && (v[q] < 0.0);
+    bool has_neg = g.any(neg);
+    double rmax = 0.0;
+    for (int q = b + g.lane; q < e; q += VS) {
+      bool off = ci[q] != r;
+      double a = v[q];
+      double cand = (off && a < 0.0) ? -a : ((off && !has_neg) ? fabs(a) : 0.0);
+      rmax = fmax(rmax, cand);
+    }
+    rmax = g.max(rmax);
+    double thr = __dmul_rn(theta, rmax);
+    int cnt = 0;
+    for (int q = b + g.lane; q < e; q += VS) {
+      bool off = ci[q] != r;
+      double a = v[q];
+      double cand = (off && a < 0.0) ? -a : ((off && !has_neg) ? fabs(a) : 0.0);
+      int8_t st = (rmax > 0.0 && cand >= thr) ? 1 : 0;
+      s[q] = st;
+      cnt |= st;
+    }
+    // only "some strong edge exists" is consumed: one atomic the first time a
+    // group sees an unset flag (a counter hit by every row serialised the kernel)
+    bool has = g.any(cnt != 0);
+    if (g.lane == 0 && has && *(volatile int *)any == 0) atomicExch(any, 1);
   }
-  for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-  double thr = __dmul_rn(theta, rmax);
-  int cnt = 0;
-  for (int q = b + lane; q < e; q += 32) {
-    bool off = ci[q] != wid;
-    double a = v[q];
-    double cand = (off && a < 0.0) ? -a : ((off && !has_neg) ? fabs(a) : 0.0);
-    int8_t st = (rmax > 0.0 && cand >= thr) ? 1 : 0;
-    s[q] = st;
-    cnt |= st;
-  }
-  // only "some strong edge exists" is consumed: one atomic the first time a
-  // warp sees an unset flag (a counter hit by every row serialised the kernel)
-  unsigned has = __ballot_sync(0xffffffffu, cnt != 0);
-  if (lane == 0 && has && *(volatile int *)any == 0) atomicExch(any, 1);
 }
 
 int64_t strength(const Csr &a, double theta, DBuf<int8_t> &s) {
@@ -147,8 +150,7 @@ int64_t strength(const Csr &a, double theta, DBuf<int8_t> &s) {
   DBuf<int> any(1);
   dzero(any.p, sizeof(int));
   if (a.nr) {
-    k_strength<<<grid_for((int64_t)a.nr * 32, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, theta,
-                                                                         s.p, any.p);
+    MG_ROWGROUP_LAUNCH(k_strength, a.nr, a.nnz, a.nr, a.rp.p, a.ci.p, a.v.p, theta, s.p, any.p);
     check_launch("strength");
   }
   int h = 0;
@@ -164,17 +166,21 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
+template <int VS>
 __global__ void k_st_count(int n, const int *rp, const int *ci, const int8_t *s, int *cnt) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= n) return;
-  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32)
-    if (s[q] && ci[q] != wid) atomicAdd(&cnt[ci[q]], 1);
+  for (RowGroup<VS> g; g.row < n; g.next()) {
+    const int r = (int)g.row;
+    for (int q = rp[r] + g.lane; q < rp[r + 1]; q += VS)
+      if (s[q] && ci[q] != r) atomicAdd(&cnt[ci[q]], 1);
+  }
 }
+template <int VS>
 __global__ void k_st_fill(int n, const int *rp, const int *ci, const int8_t *s, int *pos, int *tind) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= n) return;
-  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32)
-    if (s[q] && ci[q] != wid) tind[atomicAdd(&pos[ci[q]], 1)] = wid;
+  for (RowGroup<VS> g; g.row < n; g.next()) {
+    const int r = (int)g.row;
+    for (int q = rp[r] + g.lane; q < rp[r + 1]; q += VS)
+      if (s[q] && ci[q] != r) tind[atomicAdd(&pos[ci[q]], 1)] = r;
+  }
 }
 __global__ void k_pmis_init(int n, const int *trp, uint64_t seed, int level, double *mu, int8_t *state,
                             int *undecided) {
@@ -233,12 +239,12 @@ int pmis(const Csr &a, const int8_t *s, uint64_t seed, int level, DBuf<int8_t> &
   if (!n) return 0;
   DBuf<int> tcnt((size_t)n + 1), trp((size_t)n + 1), tpos((size_t)n);
   dzero(tcnt.p, sizeof(int) * ((size_t)n + 1));
-  k_st_count<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, tcnt.p);
+  MG_ROWGROUP_LAUNCH(k_st_count, n, a.nnz, n, a.rp.p, a.ci.p, s, tcnt.p);
   check_launch("st_count");
   int64_t nt = exclusive_scan_i32_to_i32(tcnt.p, trp.p, n);
   DBuf<int> tind((size_t)(nt ? nt : 1));
   d2d(tpos.p, trp.p, sizeof(int) * (size_t)n);
-  k_st_fill<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, tpos.p, tind.p);
+  MG_ROWGROUP_LAUNCH(k_st_fill, n, a.nnz, n, a.rp.p, a.ci.p, s, tpos.p, tind.p);
   check_launch("st_fill");
   DBuf<double> mu(n);
   DBuf<int8_t> newc(n);
@@ -280,18 +286,20 @@ __device__ __forceinline__ bool opposite(double v, double dkk) {
 }
 
 // candidate bound per row: C rows 1; F rows: strong C + sum_{strong F k} |row k|
+template <int VS>
 __global__ void k_ext_ub(int n, const int *rp, const int *ci, const int8_t *s, const int8_t *state, int *ub) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= n) return;
-  int64_t c = 0;
-  if (state[wid] != CPT)
-    for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) {
-      int j = ci[q];
-      if (j == wid || !s[q]) continue;
-      c += state[j] == FPT ? (rp[j + 1] - rp[j]) : 1;
-    }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0) ub[wid] = c > 0x3fffffff ? 0x3fffffff : (int)c;
+  for (RowGroup<VS> g; g.row < n; g.next()) {
+    const int r = (int)g.row;
+    int64_t c = 0;
+    if (state[r] != CPT)
+      for (int q = rp[r] + g.lane; q < rp[r + 1]; q += VS) {
+        int j = ci[q];
+        if (j == r || !s[q]) continue;
+        c += state[j] == FPT ? (rp[j + 1] - rp[j]) : 1;
+      }
+    c = g.sum(c);
+    if (g.lane == 0) ub[r] = c > 0x3fffffff ? 0x3fffffff : (int)c;
+  }
 }
 
 struct ExtArgs {
@@ -665,7 +673,7 @@ Csr ext_interp(const Csr &a, const int8_t *s, const int8_t *state, const int *cm
   const int big = 0x7fffffff;
   dset_i32(bad.p, {big});
   if (n) {
-    k_ext_ub<<<grid_for((int64_t)n * 32, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, state, ub.p);
+    MG_ROWGROUP_LAUNCH(k_ext_ub, n, a.nnz, n, a.rp.p, a.ci.p, s, state, ub.p);
     check_launch("ext_ub");
   }
   ExtArgs A{a.rp.p, a.ci.p, a.v.p, s, state, cmap, max_elmts, 0, cnt.p, nullptr, nullptr, nullptr, bad.p};

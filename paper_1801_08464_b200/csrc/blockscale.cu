@@ -87,39 +87,57 @@ __device__ __forceinline__ double scaled(const double *d, const double *a, int r
   return s;
 }
 
-// one thread per scalar row (cell i, var r): mode 0 count, mode 1 fill
-template <int B>
+// VS lanes per scalar row t = (cell i, var r), lane l takes blocks rp[i] + l,
+// + VS, ...; entries keep (block, column) order through a group scan of the
+// per-lane kept counts.  mode 0 count, mode 1 fill.
+template <int B, int VS>
 __global__ void k_scale_rows(int N, const int *rp, const int *ci, const double *v, const double *dinv,
                              int mode, int *cnt, const int *orp, int *oci, double *ov, int equil) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)N * B) return;
-  int i = (int)(t / B), r = (int)(t % B);
-  double d[B * B];
-#pragma unroll
-  for (int q = 0; q < B * B; ++q) d[q] = dinv[(int64_t)i * B * B + q];
-  int c0 = 0;
-  int o = mode ? orp[t] : 0;
-  for (int q = rp[i]; q < rp[i + 1]; ++q) {
-    int j = ci[q];
-    if (j == i) {
+  for (RowGroup<VS> g; g.row < (int64_t)N * B; g.next()) {
+    const int64_t t = g.row;
+    const int i = (int)(t / B), r = (int)(t % B);
+    double d[B * B];
+  #pragma unroll
+    for (int q = 0; q < B * B; ++q) d[q] = dinv[(int64_t)i * B * B + q];
+    const int qb = rp[i], qe = rp[i + 1];
+    int64_t o = mode ? orp[t] : 0;
+    int c0 = 0;
+    for (int q0 = qb; q0 < qe; q0 += VS) {
+      const int q = q0 + g.lane;
+      int kept = 0;
+      int cols[B];
+      double vals[B];
+      if (q < qe) {
+        const int j = ci[q];
+        const double *a = v + (int64_t)q * B * B;
+        if (j == i) {
+          cols[0] = i * B + r;
+          vals[0] = equil ? lambda_of<B>(a, r) : 1.0;
+          kept = 1;
+        } else {
+  #pragma unroll
+          for (int c = 0; c < B; ++c) {
+            double s = scaled<B>(d, a, r, c);
+            if (s != 0.0) { cols[kept] = j * B + c; vals[kept] = s; ++kept; }
+          }
+        }
+      }
+      int incl = kept;
+  #pragma unroll
+      for (int off = 1; off < VS; off <<= 1) {
+        int y = __shfl_up_sync(g.mask, incl, off, VS);
+        if (g.lane >= off) incl += y;
+      }
       if (mode) {
-        oci[o + c0] = i * B + r;
-        ov[o + c0] = equil ? lambda_of<B>(v + (int64_t)q * B * B, r) : 1.0;
+        const int64_t p = o + c0 + incl - kept;
+  #pragma unroll
+        for (int e = 0; e < B; ++e)
+          if (e < kept) { oci[p + e] = cols[e]; ov[p + e] = vals[e]; }
       }
-      ++c0;
-      continue;
+      c0 += g.bcast(incl, VS - 1);
     }
-    const double *a = v + (int64_t)q * B * B;
-#pragma unroll
-    for (int c = 0; c < B; ++c) {
-      double s = scaled<B>(d, a, r, c);
-      if (s != 0.0) {
-        if (mode) { oci[o + c0] = j * B + c; ov[o + c0] = s; }
-        ++c0;
-      }
-    }
+    if (!mode && g.lane == 0) cnt[t] = c0;
   }
-  if (!mode) cnt[t] = c0;
 }
 
 template <int B>
@@ -175,9 +193,11 @@ void block_scale(const Csr &a, Csr &dinv, Csr &ahat, bool equil) {
   ahat.rp.alloc((size_t)n + 1);
   auto launch = [&](int mode, int *c, const int *orp, int *oci, double *ov) {
     if (B == 2)
-      k_scale_rows<2><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, mode, c, orp, oci, ov, eq);
+      k_scale_rows<2, 8><<<rowgroup_grid(n * 8), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, mode, c, orp,
+                                                                    oci, ov, eq);
     else
-      k_scale_rows<3><<<grid_for(n, 256), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, mode, c, orp, oci, ov, eq);
+      k_scale_rows<3, 8><<<rowgroup_grid(n * 8), 256, 0, stream()>>>(N, a.rp.p, a.ci.p, a.v.p, dinv.v.p, mode, c, orp,
+                                                                    oci, ov, eq);
     check_launch("scale_rows");
   };
   launch(0, cnt.p, nullptr, nullptr, nullptr);

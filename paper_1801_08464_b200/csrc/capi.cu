@@ -162,8 +162,10 @@ int mg_ctx_destroy(mg_ctx *ctx) {
       cudaStreamDestroy(ctx->c.copy_stream);
     }
     alloc_release_cache(&ctx->c);
-    for (auto &kv : ctx->c.block_size) cudaFree(kv.first);  // blocks still owned by live handles
+    for (auto &kv : ctx->c.block_size)  // blocks still owned by live handles
+      if (!alloc_in_slab(&ctx->c, kv.first)) cudaFree(kv.first);
     ctx->c.block_size.clear();
+    alloc_release_slabs(&ctx->c);
     if (ctx->c.ev0) { cudaEventDestroy(ctx->c.ev0); cudaEventDestroy(ctx->c.ev1); }
     cudaStreamDestroy(ctx->c.stream);
   }

@@ -22,13 +22,31 @@ static size_t round_size(size_t b) {
 
 static Ctx *alloc_owner() { return g_ctx->owner ? g_ctx->owner : g_ctx; }
 
+static const size_t SLAB = (size_t)256 << 20;
+
+bool alloc_in_slab(const Ctx *c, const void *p) {
+  for (char *s : c->slabs)
+    if ((const char *)p >= s && (const char *)p < s + SLAB) return true;
+  return false;
+}
+
 void alloc_release_cache(Ctx *c) {
-  // caller holds c->amu (or no worker is running)
+  // caller holds c->amu (or no worker is running); slab-carved blocks stay pooled
   cudaDeviceSynchronize();
   for (auto &pool : c->pools)
-    for (auto &kv : pool) cudaFree(kv.second.p);
-  for (auto &pool : c->pools) pool.clear();
-  c->cached_bytes = 0;
+    for (auto it = pool.begin(); it != pool.end();) {
+      if (alloc_in_slab(c, it->second.p)) { ++it; continue; }
+      cudaFree(it->second.p);
+      c->cached_bytes -= it->first;
+      it = pool.erase(it);
+    }
+}
+
+void alloc_release_slabs(Ctx *c) {
+  for (char *s : c->slabs) cudaFree(s);
+  c->slabs.clear();
+  c->slab_cur = nullptr;
+  c->slab_left = 0;
 }
 
 void *dmalloc(size_t bytes) {
@@ -54,8 +72,54 @@ void *dmalloc(size_t bytes) {
     c->dev_bytes += (int64_t)sz;
     return p;
   }
+  // No block usable as is: take one freed on another stream and order this
+  // stream after everything that stream has enqueued so far (its last use of
+  // the block included).  A cross-stream wait is far cheaper than cudaMalloc,
+  // which can stall for tens of ms behind queued work.
+  for (auto it = pool.lower_bound(rb); it != pool.end() && it->first <= limit; ++it) {
+    const Ctx::FreeBlk &fb = it->second;
+    if (fb.freer && fb.freer != s) {
+      cudaEvent_t ev;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) break;
+      cudaEventRecord(ev, fb.freer);
+      cudaStreamWaitEvent(s, ev, 0);
+      cudaEventDestroy(ev);
+    }
+    void *p = fb.p;
+    size_t sz = it->first;
+    pool.erase(it);
+    c->cached_bytes -= sz;
+    c->block_size[p] = Ctx::BlkInfo{sz, me->pool_id};
+    c->dev_bytes += (int64_t)sz;
+    return p;
+  }
+  if (rb <= SLAB / 4) {
+    if (rb > c->slab_left) {
+      char *sl = nullptr;
+      if (cudaMalloc(&sl, SLAB) == cudaSuccess) {
+        c->slabs.push_back(sl);
+        c->slab_cur = sl;
+        c->slab_left = SLAB;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (rb <= c->slab_left) {
+      void *p = c->slab_cur;
+      c->slab_cur += rb;
+      c->slab_left -= rb;
+      c->block_size[p] = Ctx::BlkInfo{rb, me->pool_id};
+      c->dev_bytes += (int64_t)rb;
+      return p;
+    }
+  }
   void *p = nullptr;
+  static const bool alloc_log = getenv("MG_ALLOC_LOG") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMalloc(&p, rb);
+  if (alloc_log)
+    fprintf(stderr, "[mg] cudaMalloc %zu bytes (pool %d): %.3f ms\n", rb, me->pool_id,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   if (e != cudaSuccess) {
     cudaGetLastError();
     alloc_release_cache(c);
@@ -287,13 +351,33 @@ void trace(const char *what) {
 // small transfers are staged through the context's pinned buffer (a pageable
 // copy goes through the driver's shared staging path and costs more per call)
 static const size_t STAGE_MAX = 64 << 10;
+// Host->device copies up to this size are staged in pinned memory and pulled
+// by a kernel reading the mapped host buffer: every copy-engine H2D transfer
+// (pinned or not, any stream) queues behind a bulk upload in flight (an
+// asynchronous matrix upload on the copy stream), a kernel load does not.
+static const size_t STAGE_H2D_MAX = 16 << 20;
+
+__global__ void k_pull_host(uint4 *__restrict__ dst, const uint4 *__restrict__ src, int64_t n16, uint8_t *dtail,
+                            const uint8_t *stail, int ntail) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && (int)threadIdx.x < ntail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
 
 void h2d(void *dst, const void *src, size_t bytes) {
   if (!bytes) return;
-  if (bytes <= STAGE_MAX) {
-    void *hs = host_scratch((bytes + 7) / 8);
+  if (bytes <= STAGE_H2D_MAX) {
+    uint8_t *hs = (uint8_t *)host_scratch((bytes + 7) / 8);
     memcpy(hs, src, bytes);
-    MG_CUDA(cudaMemcpyAsync(dst, hs, bytes, cudaMemcpyHostToDevice, g_ctx->stream));
+    if (((uintptr_t)dst & 15) == 0) {
+      int64_t n16 = (int64_t)(bytes / 16);
+      int ntail = (int)(bytes - (size_t)n16 * 16);
+      k_pull_host<<<grid_for(n16 ? n16 : 1, 256, 256), 256, 0, g_ctx->stream>>>(
+          (uint4 *)dst, (const uint4 *)hs, n16, (uint8_t *)dst + n16 * 16, hs + n16 * 16, ntail);
+      check_launch("pull_host");
+    } else {
+      MG_CUDA(cudaMemcpyAsync(dst, hs, bytes, cudaMemcpyHostToDevice, g_ctx->stream));
+    }
   } else {
     MG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, g_ctx->stream));
   }

@@ -70,6 +70,12 @@ struct Ctx {
   std::vector<std::multimap<size_t, FreeBlk>> pools{1};
   std::unordered_map<void *, BlkInfo> block_size;
   size_t cached_bytes = 0;
+  // slabs: pool misses up to SLAB/4 bytes are carved from 256 MB slabs
+  // (bump pointer) instead of separate cudaMalloc calls; carved blocks are
+  // pooled like any other and released with their slab at context teardown
+  std::vector<char *> slabs;
+  char *slab_cur = nullptr;
+  size_t slab_left = 0;
   int pool_id = 0;          // this context's home pool
   int64_t epoch = 0;        // parent: number of forks so far
   int64_t fork_epoch = 0;   // worker: parent epoch at its fork
@@ -101,6 +107,8 @@ class TaskGroup {
 };
 
 void alloc_release_cache(Ctx *c);
+void alloc_release_slabs(Ctx *c);
+bool alloc_in_slab(const Ctx *c, const void *p);
 
 inline cudaStream_t stream() { return g_ctx->stream; }
 
@@ -241,5 +249,62 @@ int64_t exclusive_scan_i32_to_i32(const int *in, int *out, int n);
 int64_t exclusive_scan_i32_to_i64(const int *in, int64_t *out, int n);
 int64_t reduce_sum_i32(const int *in, int n);
 int64_t count_u8(const uint8_t *in, int n);
+
+// Row groups for the setup kernels that walk one CSR row per group: VS lanes
+// (a power of two <= 32) per row, so short rows do not leave most of a warp
+// idle on a chain of dependent loads.  Warp primitives take the group's lane
+// mask; bits / sources are group-relative.
+template <int VS>
+struct RowGroup {
+  int64_t row;
+  int lane, base;
+  unsigned mask;
+  __device__ __forceinline__ RowGroup() {
+    row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VS;
+    lane = threadIdx.x & (VS - 1);
+    base = (threadIdx.x & 31) & ~(VS - 1);
+    mask = VS == 32 ? 0xffffffffu : (((1u << (VS & 31)) - 1u) << base);
+  }
+  // grid-stride: the launch is capped at a few blocks per SM (block launch
+  // overhead, not memory, bounds a grid of one tiny block per 8-32 rows)
+  __device__ __forceinline__ void next() { row += ((int64_t)gridDim.x * blockDim.x) / VS; }
+  __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(mask, p) >> base; }
+  __device__ __forceinline__ bool any(bool p) const { return ballot(p) != 0; }
+  template <class T>
+  __device__ __forceinline__ T sum(T v) const {
+#pragma unroll
+    for (int o = VS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, VS);
+    return v;
+  }
+  __device__ __forceinline__ double max(double v) const {
+#pragma unroll
+    for (int o = VS / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(mask, v, o, VS));
+    return v;
+  }
+  template <class T>
+  __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(mask, v, src, VS); }
+  // lanes below this one among the set bits of a group ballot
+  __device__ __forceinline__ int rank(unsigned bits) const { return __popc(bits & ((1u << lane) - 1u)); }
+};
+
+// lanes per row from the average row length
+inline int row_group_lanes(int64_t nnz, int64_t rows) {
+  double avg = rows ? (double)nnz / (double)rows : 0.0;
+  return avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+}
+
+inline int rowgroup_grid(int64_t threads) { return grid_for(threads, 256, g_ctx->num_sms * 8); }
+
+// launch KERNEL<VS> over `rows` rows with VS = row_group_lanes(nnz, rows)
+#define MG_ROWGROUP_LAUNCH(KERNEL, rows, nnz, ...)                                                   \
+  do {                                                                                              \
+    int64_t rg_rows_ = (rows);                                                                      \
+    switch (::mg::row_group_lanes((nnz), rg_rows_)) {                                               \
+      case 4: KERNEL<4><<<::mg::rowgroup_grid(rg_rows_ * 4), 256, 0, ::mg::stream()>>>(__VA_ARGS__); break;   \
+      case 8: KERNEL<8><<<::mg::rowgroup_grid(rg_rows_ * 8), 256, 0, ::mg::stream()>>>(__VA_ARGS__); break;   \
+      case 16: KERNEL<16><<<::mg::rowgroup_grid(rg_rows_ * 16), 256, 0, ::mg::stream()>>>(__VA_ARGS__); break; \
+      default: KERNEL<32><<<::mg::rowgroup_grid(rg_rows_ * 32), 256, 0, ::mg::stream()>>>(__VA_ARGS__); break; \
+    }                                                                                               \
+  } while (0)
 
 }  // namespace mg

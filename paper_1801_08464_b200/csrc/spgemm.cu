@@ -264,38 +264,42 @@ __global__ void k_spgemm_fill_g(int nrows, const int *rows, const int64_t *goff,
   fill_row(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
 }
 
-// compaction: drop exact zeros, keep order (warp per row)
+// compaction: drop exact zeros, keep order (VS-lane group per row)
+template <int VS>
 __global__ void k_compact(int m, const int64_t *tmp_rp, const int *tci, const double *tv, const int *rp,
                           int *ci, double *v) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= m) return;
-  int64_t s = tmp_rp[wid], e = tmp_rp[wid + 1];
-  int o = rp[wid];
-  for (int64_t q0 = s; q0 < e; q0 += 32) {
-    int64_t q = q0 + lane;
-    double val = q < e ? tv[q] : 0.0;
-    bool keep = q < e && val != 0.0;
-    unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      int p = o + __popc(bal & ((1u << lane) - 1));
-      ci[p] = tci[q];
-      v[p] = val;
+  for (RowGroup<VS> g; g.row < m; g.next()) {
+    const int r = (int)g.row;
+    int64_t s = tmp_rp[r], e = tmp_rp[r + 1];
+    int o = rp[r];
+    for (int64_t q0 = s; q0 < e; q0 += VS) {
+      int64_t q = q0 + g.lane;
+      double val = q < e ? tv[q] : 0.0;
+      bool keep = q < e && val != 0.0;
+      unsigned bal = g.ballot(keep);
+      if (keep) {
+        int p = o + g.rank(bal);
+        ci[p] = tci[q];
+        v[p] = val;
+      }
+      o += __popc(bal);
     }
-    o += __popc(bal);
   }
 }
 
 // per-row product upper bound
+template <int VS>
 __global__ void k_row_ub(int m, const int *arp, const int *aci, const int *brp, int *ub) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= m) return;
-  int64_t s = 0;
-  for (int q = arp[wid] + lane; q < arp[wid + 1]; q += 32) {
-    int j = aci[q];
-    s += brp[j + 1] - brp[j];
+  for (RowGroup<VS> g; g.row < m; g.next()) {
+    const int r = (int)g.row;
+    int64_t s = 0;
+    for (int q = arp[r] + g.lane; q < arp[r + 1]; q += VS) {
+      int j = aci[q];
+      s += brp[j + 1] - brp[j];
+    }
+    s = g.sum(s);
+    if (g.lane == 0) ub[r] = s > 0x3fffffff ? 0x3fffffff : (int)s;
   }
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) ub[wid] = s > 0x3fffffff ? 0x3fffffff : (int)s;
 }
 
 __device__ __forceinline__ int bin_of(int v) {
@@ -416,7 +420,7 @@ Csr spgemm(const Csr &a, const Csr &b) {
     return c;
   }
   DBuf<int> ub(m), cnt(m), nz(m);
-  k_row_ub<<<grid_for((int64_t)m * 32, 256), 256, 0, stream()>>>(m, a.rp.p, a.ci.p, b.rp.p, ub.p);
+  MG_ROWGROUP_LAUNCH(k_row_ub, m, a.nnz, m, a.rp.p, a.ci.p, b.rp.p, ub.p);
   check_launch("row_ub");
   {
     // count pass, tables sized by the product count (all keys could be distinct)
@@ -476,17 +480,19 @@ Csr spgemm(const Csr &a, const Csr &b) {
   } else {
     c.ci.alloc((size_t)kept);
     c.v.alloc((size_t)kept);
-    k_compact<<<grid_for((int64_t)m * 32, 256), 256, 0, stream()>>>(m, trp.p, tci.p, tv.p, c.rp.p, c.ci.p, c.v.p);
+    MG_ROWGROUP_LAUNCH(k_compact, m, total, m, trp.p, tci.p, tv.p, c.rp.p, c.ci.p, c.v.p);
     check_launch("compact");
   }
   return c;
 }
 
 // ---- transpose (stable: rows of A^T have ascending columns) -----------------
+template <int VS>
 __global__ void k_row_ids(int m, const int *rp, int *rid) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= m) return;
-  for (int q = rp[wid] + lane; q < rp[wid + 1]; q += 32) rid[q] = wid;
+  for (RowGroup<VS> g; g.row < m; g.next()) {
+    const int r = (int)g.row;
+    for (int q = rp[r] + g.lane; q < rp[r + 1]; q += VS) rid[q] = r;
+  }
 }
 __global__ void k_iota(int *a, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -519,7 +525,7 @@ Csr transpose(const Csr &a) {
   exclusive_scan_i32_to_i32(cnt.p, t.rp.p, a.nc);
   if (!nnz) return t;
   DBuf<int> rid((size_t)nnz), idx((size_t)nnz), keys_out((size_t)nnz), perm((size_t)nnz);
-  k_row_ids<<<grid_for((int64_t)a.nr * 32, 256), 256, 0, stream()>>>(a.nr, a.rp.p, rid.p);
+  MG_ROWGROUP_LAUNCH(k_row_ids, a.nr, a.nnz, a.nr, a.rp.p, rid.p);
   check_launch("row_ids");
   k_iota<<<grid_for(nnz, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(idx.p, nnz);
   check_launch("iota");
@@ -539,32 +545,35 @@ Csr transpose(const Csr &a) {
 }
 
 // ---- extract A[rows][:, cols] (keeps stored zeros) ---------------------------
+template <int VS>
 __global__ void k_extract_count(int nr, const int *rows, const int *rp, const int *ci, const int *cmap,
                                 int *cnt) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= nr) return;
-  int r = rows[wid];
-  int c = 0;
-  for (int q = rp[r] + lane; q < rp[r + 1]; q += 32) c += cmap[ci[q]] >= 0;
-  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-  if (lane == 0) cnt[wid] = c;
+  for (RowGroup<VS> g; g.row < nr; g.next()) {
+    int r = rows[g.row];
+    int c = 0;
+    for (int q = rp[r] + g.lane; q < rp[r + 1]; q += VS) c += cmap[ci[q]] >= 0;
+    c = g.sum(c);
+    if (g.lane == 0) cnt[g.row] = c;
+  }
 }
+template <int VS>
 __global__ void k_extract_fill(int nr, const int *rows, const int *rp, const int *ci, const double *v,
                                const int *cmap, const int *orp, int *oci, double *ov) {
-  int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= nr) return;
-  int r = rows[wid];
-  int o = orp[wid];
-  for (int q0 = rp[r]; q0 < rp[r + 1]; q0 += 32) {
-    int q = q0 + lane;
-    int m = q < rp[r + 1] ? cmap[ci[q]] : -1;
-    unsigned bal = __ballot_sync(0xffffffffu, m >= 0);
-    if (m >= 0) {
-      int p = o + __popc(bal & ((1u << lane) - 1));
-      oci[p] = m;
-      ov[p] = v[q];
+  for (RowGroup<VS> g; g.row < nr; g.next()) {
+    int r = rows[g.row];
+    int o = orp[g.row];
+    const int e = rp[r + 1];
+    for (int q0 = rp[r]; q0 < e; q0 += VS) {
+      int q = q0 + g.lane;
+      int m = q < e ? cmap[ci[q]] : -1;
+      unsigned bal = g.ballot(m >= 0);
+      if (m >= 0) {
+        int p = o + g.rank(bal);
+        oci[p] = m;
+        ov[p] = v[q];
+      }
+      o += __popc(bal);
     }
-    o += __popc(bal);
   }
 }
 
@@ -575,17 +584,16 @@ Csr extract(const Csr &a, const int *rows_dev, int nr, const int *cmap_dev, int 
   o.rp.alloc((size_t)nr + 1);
   DBuf<int> cnt((size_t)nr + 1);
   if (nr) {
-    k_extract_count<<<grid_for((int64_t)nr * 32, 256), 256, 0, stream()>>>(nr, rows_dev, a.rp.p, a.ci.p,
-                                                                            cmap_dev, cnt.p);
+    MG_ROWGROUP_LAUNCH(k_extract_count, nr, a.nr ? (int64_t)((double)a.nnz * nr / a.nr) : 0, nr, rows_dev, a.rp.p,
+                       a.ci.p, cmap_dev, cnt.p);
     check_launch("extract_count");
   }
   o.nnz = exclusive_scan_i32_to_i32(cnt.p, o.rp.p, nr);
   o.ci.alloc((size_t)o.nnz);
   o.v.alloc((size_t)o.nnz);
   if (nr && o.nnz) {
-    k_extract_fill<<<grid_for((int64_t)nr * 32, 256), 256, 0, stream()>>>(nr, rows_dev, a.rp.p, a.ci.p,
-                                                                           a.v.p, cmap_dev, o.rp.p, o.ci.p,
-                                                                           o.v.p);
+    MG_ROWGROUP_LAUNCH(k_extract_fill, nr, a.nr ? (int64_t)((double)a.nnz * nr / a.nr) : 0, nr, rows_dev, a.rp.p,
+                       a.ci.p, a.v.p, cmap_dev, o.rp.p, o.ci.p, o.v.p);
     check_launch("extract_fill");
   }
   return o;
