@@ -80,6 +80,12 @@ int mg_mat_free(mg_ctx *ctx, mg_mat *m);
 /* y = A x (sparse.py:174-178 spmv; the GMRES operator `a @ v`, linsolve.py:100) */
 int mg_spmv(mg_ctx *ctx, const mg_mat *a, const double *x, double *y);
 int mg_spmv_dev(mg_ctx *ctx, const mg_mat *a, const double *x_dev, double *y_dev);
+/* Solve-phase layout the SpMV kernels use for `a` (built on first use; no
+   reference counterpart, the layout is an implementation detail exposed for
+   tests and profiling): *sell = 1 for a SELL-32 copy, 0 for plain CSR/BSR;
+   *index_bytes = stored bytes per column index (4 int32; 2 / 1 for the
+   lossless int16 / u8-dictionary column codes of large stencil-like operators) */
+int mg_spmv_layout(mg_ctx *ctx, const mg_mat *a, int *sell, int *index_bytes);
 /* C = A B with scipy csr_matmat semantics (sparse.py:193-196): exact zeros dropped */
 int mg_matmul(mg_ctx *ctx, const mg_mat *a, const mg_mat *b, mg_mat **out);
 /* R (A P) (sparse.py:199-203) */

@@ -263,6 +263,15 @@ int mg_spmv_dev(mg_ctx *ctx, const mg_mat *a, const double *x_dev, double *y_dev
   return guard(ctx, [&] { spmv(C(a), x_dev, y_dev); });
 }
 
+int mg_spmv_layout(mg_ctx *ctx, const mg_mat *a, int *sell, int *index_bytes) {
+  return guard(ctx, [&] {
+    const Csr &c = C(a);
+    prepare_spmv(c);
+    if (sell) *sell = c.plan->sell ? 1 : 0;
+    if (index_bytes) *index_bytes = c.plan->sell ? c.plan->idx_bytes() : 4;
+  });
+}
+
 int mg_matmul(mg_ctx *ctx, const mg_mat *a, const mg_mat *b, mg_mat **out) {
   return guard(ctx, [&] {
     auto *m = new mg_mat();

@@ -194,8 +194,17 @@ struct SpmvPlan {
   bool sell = false;
   DBuf<int> sptr;            // slice start (elements), nslices + 1
   DBuf<int> rlen;            // row lengths
-  DBuf<int> sci;
+  DBuf<int> sci;             // int32 columns (ik == 0)
   DBuf<double> sv;
+  // lossless column compression (spmv.cu build_codes): col = anchor(row) + code,
+  // anchor(row) = (row * mul) >> 32.  ik 1: u8 codes into `dict` (<= 256 distinct
+  // codes), ik 2: int16 codes; packed 4 (2) per 32-bit word, word (k / 4, lane)
+  // of a slice.  Same entries in the same order: results bit-identical.
+  int ik = 0;
+  unsigned long long mul = 0;
+  DBuf<unsigned> scode;
+  DBuf<int> dict;
+  int idx_bytes() const { return ik == 1 ? 1 : ik == 2 ? 2 : 4; }
 };
 
 // Device CSR; b > 1 means block CSR with b*b row-major values per entry.
@@ -215,8 +224,11 @@ struct Csr {
     ci.alloc((size_t)nnz);
     v.alloc((size_t)nnz * b * b);
   }
-  double bytes_spmv() const {  // algorithmic bytes of y = A x
-    double vb = (double)nnz * (8.0 * b * b + 4.0) + 4.0 * (nr + 1);
+  // algorithmic bytes of y = A x in the stored format: int32
+  // columns, or 1 / 2 B per entry when the SELL copy is column-compressed
+  double bytes_spmv() const {
+    const double ib = plan && plan->sell ? plan->idx_bytes() : 4.0;
+    double vb = (double)nnz * (8.0 * b * b + ib) + 4.0 * (nr + 1);
     return vb + 8.0 * b * nc + 8.0 * b * nr;
   }
 };

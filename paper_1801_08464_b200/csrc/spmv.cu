@@ -87,14 +87,50 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ row
 }
 
 // ---- SELL-32: one thread per row, loads coalesced across the 32 rows of a slice ----
-template <int UNR, class Epi, class XG>
+// IK selects the column encoding (SpmvPlan::ik): 0 int32, 1 u8 code -> dict, 2 int16
+// code; codes are relative to anchor(row) = (row * mul) >> 32 and packed 4 / 2 per
+// 32-bit word so that one word load per thread covers 4 / 2 entries (a coalesced
+// 128 B warp access).  Slice lengths are multiples of 4 (build_sell).
+__device__ __forceinline__ int sell_anchor(int row, unsigned long long mul) {
+  return (int)(((unsigned long long)row * mul) >> 32);
+}
+template <int IK>
+__device__ __forceinline__ void sell_cols4(const void *__restrict__ ci, int base, int wbase, int k, int anc,
+                                           const int *tbl, int (&cc)[4]) {
+  if (IK == 0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cc[u] = __ldcs(static_cast<const int *>(ci) + base + (k + u) * 32);
+  } else if (IK == 1) {
+    const unsigned w = __ldcs(static_cast<const unsigned *>(ci) + wbase + (k >> 2) * 32);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cc[u] = anc + tbl[(w >> (8 * u)) & 255u];
+  } else {
+    const unsigned *p = static_cast<const unsigned *>(ci) + wbase + (k >> 1) * 32;
+    const unsigned w0 = __ldcs(p), w1 = __ldcs(p + 32);
+    cc[0] = anc + (int)(short)(w0 & 0xffffu);
+    cc[1] = anc + (int)(short)(w0 >> 16);
+    cc[2] = anc + (int)(short)(w1 & 0xffffu);
+    cc[3] = anc + (int)(short)(w1 >> 16);
+  }
+}
+template <int UNR, int IK, class Epi, class XG>
 __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sptr, const int *__restrict__ rlen,
-                                              const int *__restrict__ ci, const double *__restrict__ v,
+                                              const void *__restrict__ ci, const int *__restrict__ dict,
+                                              unsigned long long mul, const double *__restrict__ v,
                                               XG x, Epi epi) {
+  static_assert(UNR % 4 == 0, "SELL unroll is a multiple of the 4-entry code word");
+  __shared__ int tbl[IK == 1 ? 256 : 1];
   PDL_ENTRY();
+  if (IK == 1) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) tbl[i] = __ldg(dict + i);
+    __syncthreads();
+  }
   int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= nr) return;
-  const int base = __ldg(sptr + (row >> 5)) + (row & 31);
+  const int sbase = __ldg(sptr + (row >> 5));
+  const int base = sbase + (row & 31);
+  const int wbase = (IK == 1 ? (sbase >> 2) : (sbase >> 1)) + (row & 31);
+  const int anc = IK ? sell_anchor(row, mul) : 0;
   const int len = __ldg(rlen + row);
   double sum = 0.0;
   int k = 0;
@@ -102,19 +138,39 @@ __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sp
     double vv[UNR];
     int cc[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      vv[u] = __ldcs(v + base + (k + u) * 32);
-      cc[u] = __ldcs(ci + base + (k + u) * 32);
+    for (int u = 0; u < UNR; ++u) vv[u] = __ldcs(v + base + (k + u) * 32);
+#pragma unroll
+    for (int q = 0; q < UNR / 4; ++q) {
+      int c4[4];
+      sell_cols4<IK>(ci, base, wbase, k + 4 * q, anc, tbl, c4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cc[4 * q + u] = c4[u];
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) sum += vv[u] * x(cc[u]);
   }
-  for (; k < len; ++k) sum += __ldcs(v + base + k * 32) * x(__ldcs(ci + base + k * 32));
+  for (; k < len; k += 4) {
+    const int m = len - k;  // 1..UNR-1 entries left; the code word is padded
+    double vv[4];
+    int cc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vv[u] = u < m ? __ldcs(v + base + (k + u) * 32) : 0.0;
+    if (IK == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cc[u] = u < m ? __ldcs(static_cast<const int *>(ci) + base + (k + u) * 32) : 0;
+    } else {
+      sell_cols4<IK>(ci, base, wbase, k, anc, tbl, cc);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u < m) sum += vv[u] * x(cc[u]);
+  }
   epi(row, sum);
 }
 
-// per slice: max row length (warp per slice)
-__global__ void k_sell_len(int nr, int ns, const int *rp, int *rlen, int *slen) {
+// per slice: max row length (warp per slice); Q rounds the slice length up to a
+// multiple of Q entries (4 for the scalar SELL copy: whole code words)
+__global__ void k_sell_len(int nr, int ns, const int *rp, int *rlen, int *slen, int q) {
   int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (s >= ns) return;
   int row = s * 32 + lane;
@@ -122,7 +178,7 @@ __global__ void k_sell_len(int nr, int ns, const int *rp, int *rlen, int *slen) 
   if (row < nr) rlen[row] = len;
   int m = len;
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) slen[s] = m * 32;
+  if (lane == 0) slen[s] = (m + q - 1) / q * q * 32;
 }
 __global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *v, const int *sptr, int *sci,
                             double *sv) {
@@ -131,9 +187,149 @@ __global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *
   int base = sptr[row >> 5] + (row & 31);
   int s = rp[row], e = rp[row + 1];
   for (int k = 0; k < e - s; ++k) {
-    sci[base + k * 32] = ci[s + k];
+    if (sci) sci[base + k * 32] = ci[s + k];
     sv[base + k * 32] = v[s + k];
   }
+}
+
+// ---- column compression (SpmvPlan::ik) ------------------------------------------
+// One pass over the columns: range of code = col - anchor(row) (warp-reduced
+// atomics) and a bitmap of the codes inside [-CWIN, CWIN) (read-before-atomicOr:
+// the few distinct codes of a stencil operator are set once, then only read).
+constexpr int CWIN = 1 << 20;
+constexpr int CWORDS = (2 * CWIN) / 32;
+__global__ void k_code_stats(int nr, const int *__restrict__ rp, const int *__restrict__ ci,
+                             unsigned long long mul, unsigned *bm, int *mm) {
+  const int lane = threadIdx.x & 7;
+  const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3);
+  const int ng = (int)(((int64_t)gridDim.x * blockDim.x) >> 3);
+  int lo = INT_MAX, hi = INT_MIN;
+  for (int row = g0; row < nr; row += ng) {
+    const int anc = sell_anchor(row, mul);
+    const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
+    for (int k = s + lane; k < e; k += 8) {
+      const int d = __ldg(ci + k) - anc;
+      lo = min(lo, d);
+      hi = max(hi, d);
+      if (d >= -CWIN && d < CWIN) {
+        const unsigned t = (unsigned)(d + CWIN), bit = 1u << (t & 31);
+        if (!(__ldcg(bm + (t >> 5)) & bit)) atomicOr(bm + (t >> 5), bit);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+// per-word popcounts -> exclusive prefix (one block), the distinct count into
+// mm[2] and the code table dict[rank] = code for the first 256 codes (ascending)
+__global__ void __launch_bounds__(1024) k_code_dict(const unsigned *bm, int *wpre, int *mm, int *dict) {
+  __shared__ int part[1024];
+  constexpr int PER = CWORDS / 1024;
+  const int t = threadIdx.x;
+  int c = 0;
+  for (int i = 0; i < PER; ++i) c += __popc(bm[t * PER + i]);
+  part[t] = c;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    int v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int run = part[t] - c;
+  for (int i = 0; i < PER; ++i) {
+    const int w = t * PER + i;
+    unsigned bits = bm[w];
+    wpre[w] = run;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (run < 256) dict[run] = w * 32 + b - CWIN;
+      ++run;
+    }
+  }
+  if (t == 1023) mm[2] = part[1023];
+}
+// codes of row `row` packed into its slice words (thread per row)
+template <int IK>
+__global__ void k_code_fill(int nr, const int *rp, const int *ci, const int *sptr, unsigned long long mul,
+                            const unsigned *bm, const int *wpre, unsigned *code) {
+  int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nr) return;
+  constexpr int PW = IK == 1 ? 4 : 2;  // codes per word
+  const int sbase = sptr[row >> 5];
+  unsigned *out = code + (sbase / PW) + (row & 31);
+  const int anc = sell_anchor(row, mul);
+  const int s = rp[row], e = rp[row + 1];
+  unsigned w = 0;
+  for (int k = 0; k < e - s; ++k) {
+    const int d = ci[s + k] - anc;
+    unsigned c;
+    if (IK == 1) {
+      const unsigned t = (unsigned)(d + CWIN);
+      c = (unsigned)(wpre[t >> 5] + __popc(bm[t >> 5] & ((1u << (t & 31)) - 1u)));
+    } else {
+      c = (unsigned)d & 0xffffu;
+    }
+    w |= c << ((k % PW) * (32 / PW));
+    if (k % PW == PW - 1) {
+      out[(k / PW) * 32] = w;
+      w = 0;
+    }
+  }
+  if ((e - s) % PW) out[((e - s) / PW) * 32] = w;
+}
+
+static int code_mode() {  // MG_SELL_CODES=0 keeps int32 columns
+  static int m = -1;
+  if (m < 0) {
+    const char *e = getenv("MG_SELL_CODES");
+    m = e ? atoi(e) : 1;
+  }
+  return m;
+}
+
+// choose and build the column encoding of a SELL copy (one host round trip)
+static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
+  pl.ik = 0;
+  if (!code_mode() || a.nr == 0 || a.nnz == 0) return;
+  pl.mul = (unsigned long long)(((unsigned __int128)(unsigned)a.nc << 32) / (unsigned)a.nr);
+  DBuf<unsigned> bm(CWORDS);
+  DBuf<int> wpre(CWORDS), mm(3);
+  MG_CUDA(cudaMemsetAsync(bm.p, 0, CWORDS * sizeof(unsigned), stream()));
+  const int init[3] = {INT_MAX, INT_MIN, 0};
+  h2d(mm.p, init, sizeof(init));
+  pl.dict.alloc(256);
+  MG_CUDA(cudaMemsetAsync(pl.dict.p, 0, 256 * sizeof(int), stream()));
+  k_code_stats<<<grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(
+      a.nr, a.rp.p, a.ci.p, pl.mul, bm.p, mm.p);
+  check_launch("code_stats");
+  k_code_dict<<<1, 1024, 0, stream()>>>(bm.p, wpre.p, mm.p, pl.dict.p);
+  check_launch("code_dict");
+  int st[3];
+  d2h(st, mm.p, sizeof(st));
+  const bool in_win = st[0] >= -CWIN && st[1] < CWIN;
+  if (in_win && st[2] <= 256) pl.ik = 1;
+  else if (st[0] >= -32768 && st[1] <= 32767) pl.ik = 2;
+  if (!pl.ik) {
+    pl.dict.release();
+    return;
+  }
+  if (pl.ik != 1) pl.dict.release();
+  pl.scode.alloc((size_t)(padded / (pl.ik == 1 ? 4 : 2)));
+  if (pl.ik == 1)
+    k_code_fill<1><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.mul, bm.p,
+                                                              wpre.p, pl.scode.p);
+  else
+    k_code_fill<2><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.mul, bm.p,
+                                                              wpre.p, pl.scode.p);
+  check_launch("code_fill");
 }
 
 static double sell_min_avg() {
@@ -149,7 +345,7 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   int ns = (a.nr + 31) / 32;
   DBuf<int> slen((size_t)ns + 1);
   pl.rlen.alloc(a.nr);
-  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p);
+  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p, 4);
   check_launch("sell_len");
   DBuf<int64_t> sp64((size_t)ns + 1);
   int64_t padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
@@ -169,13 +365,15 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
     cap_short = e ? atof(e) : 2.0;
   }
   double cap = avg <= 16.0 ? cap_short : cap_long;
-  if (padded > (int64_t)(cap * (double)a.nnz) + 4096 || padded > 2000000000LL) {
+  // (+ the rounding of slice lengths to whole code words: at most 3 x 32 per slice)
+  if (padded > (int64_t)(cap * (double)a.nnz) + 4096 + 96LL * ns || padded > 2000000000LL) {
     pl.rlen.release();
     return;
   }
   pl.sptr.alloc((size_t)ns + 1);
   exclusive_scan_i32_to_i32(slen.p, pl.sptr.p, ns);
-  pl.sci.alloc((size_t)padded);
+  build_codes(a, pl, padded);
+  if (!pl.ik) pl.sci.alloc((size_t)padded);
   pl.sv.alloc((size_t)padded);
   k_sell_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, pl.sptr.p, pl.sci.p, pl.sv.p);
   check_launch("sell_fill");
@@ -268,7 +466,7 @@ static void build_bsell(const Csr &a, SpmvPlan &pl) {
   int ns = (a.nr + 31) / 32;
   DBuf<int> slen((size_t)ns + 1);
   pl.rlen.alloc(a.nr);
-  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p);
+  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p, 1);
   check_launch("bsell_len");
   DBuf<int64_t> sp64((size_t)ns + 1);
   int64_t padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
@@ -390,12 +588,20 @@ static void launch_csr(const Csr &a, XG x, Epi epi) {
   prepare_spmv(a);
   const SpmvPlan &pl = *a.plan;
   if (pl.sell) {
-    if (avg > 64)
-      launch_pdl(k_sell<8, Epi, XG>, grid_for(a.nr, 128), 128, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x,
-                 epi);
-    else
-      launch_pdl(k_sell<4, Epi, XG>, grid_for(a.nr, 256), 256, 0, a.nr, pl.sptr.p, pl.rlen.p, pl.sci.p, pl.sv.p, x,
-                 epi);
+    const void *ci = pl.ik ? (const void *)pl.scode.p : (const void *)pl.sci.p;
+#define LAUNCH_SELL(UNR, T, IK) \
+  launch_pdl(k_sell<UNR, IK, Epi, XG>, grid_for(a.nr, T), T, 0, a.nr, pl.sptr.p, pl.rlen.p, ci, pl.dict.p, pl.mul, \
+             pl.sv.p, x, epi)
+    if (avg > 64) {
+      if (pl.ik == 1) LAUNCH_SELL(8, 128, 1);
+      else if (pl.ik == 2) LAUNCH_SELL(8, 128, 2);
+      else LAUNCH_SELL(8, 128, 0);
+    } else {
+      if (pl.ik == 1) LAUNCH_SELL(4, 256, 1);
+      else if (pl.ik == 2) LAUNCH_SELL(4, 256, 2);
+      else LAUNCH_SELL(4, 256, 0);
+    }
+#undef LAUNCH_SELL
     check_launch("sell spmv");
     return;
   }

@@ -79,6 +79,12 @@ class DeviceMatrix:
             self._info = (nr.value, nc.value, nnz.value, b.value)
         return self._info
 
+    def spmv_layout(self):
+        """(sell, index_bytes) of the solve-phase SpMV copy (mg_spmv_layout)."""
+        sell, ib = _lib.c_int(), _lib.c_int()
+        self.ctx.call("mg_spmv_layout", self.h, _lib.ctypes.byref(sell), _lib.ctypes.byref(ib))
+        return bool(sell.value), ib.value
+
     @property
     def block_size(self):
         return self._load_info()[3]

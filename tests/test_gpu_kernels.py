@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from helpers import assert_bitwise, assert_close_csr, poisson2d, rand_csr, relerr
+from helpers import assert_bitwise, assert_close_csr, poisson2d, poisson3d, rand_csr, relerr
 from oracle import blockscale as obs
 from oracle import mgr as omgr
 from paper_1801_08464_b200 import mgr as gmgr
@@ -33,6 +33,45 @@ def test_spmv_matches_scipy(gpu, seed):
         a = rand_csr(rng, n, m, dens)
         x = rng.standard_normal(m)
         assert relerr(gsp.spmv(a, x), a @ x) <= 1e-14
+
+
+def _stencil_rows(rng, nr, nc, offsets, anchor, lmin=1, lmax=None):
+    """Rows of random length (lmin..len(offsets)) over a sorted random subset of
+    anchor(row) + offsets, clipped to [0, nc): exercises every SELL tail length."""
+    indptr, cols = [0], []
+    for r in range(nr):
+        k = rng.integers(lmin, (lmax or len(offsets)) + 1)
+        c = np.unique(anchor(r) + rng.choice(offsets, size=k, replace=False))
+        c = c[(c >= 0) & (c < nc)]
+        cols.append(c)
+        indptr.append(indptr[-1] + len(c))
+    cols = np.concatenate(cols)
+    return sp.csr_matrix((rng.standard_normal(len(cols)), cols, np.array(indptr)), shape=(nr, nc))
+
+
+@pytest.mark.parametrize("case,want_ib", [("stencil", 1), ("r_shape", 1), ("p_shape", 1),
+                                          ("band", 2), ("scattered", 4)])
+def test_spmv_sell_column_codes_bitwise(gpu, case, want_ib):
+    """SELL-32 copies (>= 32768 rows) with u8-dictionary / int16 / int32 columns:
+    same entries in the same order, so y is bit-identical to scipy's row sums."""
+    rng = np.random.default_rng(7)
+    n = 40000
+    if case == "stencil":
+        a = poisson3d(34)  # 39304 rows, 7 codes
+        a.data[:] = rng.standard_normal(a.nnz)
+    elif case == "r_shape":  # nc = 2 nr: anchor(row) = 2 row
+        a = _stencil_rows(rng, n, 2 * n, np.array([-70, -2, 0, 1, 2, 3, 70, 71]), lambda r: 2 * r)
+    elif case == "p_shape":  # nr = 2 nc: anchor(row) = row // 2
+        a = _stencil_rows(rng, n, n // 2, np.array([-35, -1, 0, 1, 35]), lambda r: r // 2, lmin=3)
+    elif case == "band":  # > 256 distinct codes, all within int16
+        a = _stencil_rows(rng, n, n, rng.choice(np.arange(-30000, 30000), 400, replace=False), lambda r: r, 4, 12)
+    else:  # columns anywhere: int32
+        a = rand_csr(rng, n, n, 12.0 / n)
+    a.sort_indices()
+    d = gsp.DeviceMatrix.from_host(a)
+    assert d.spmv_layout() == (True, want_ib)
+    x = rng.standard_normal(a.shape[1])
+    np.testing.assert_array_equal(gsp.spmv(d, x), a @ x)
 
 
 def test_spmv_dimension_mismatch(gpu):

@@ -88,7 +88,9 @@ def test_empty_levels_skipped(gpu):
     assert h.level_dims() == [20, 15]
 
 
-@pytest.mark.parametrize("cfg,edge", [(1, 24), (2, 10), (3, 10), (4, 6)])
+# 32^3 / 40^3: operators with >= 32768 rows run on the SELL-32 copies with
+# compressed column codes (spmv.cu), so mgr_apply covers that path too
+@pytest.mark.parametrize("cfg,edge", [(1, 24), (2, 10), (3, 10), (4, 6), (2, 32), (3, 32), (4, 40)])
 def test_synthetic_hierarchy_bitwise(gpu, cfg, edge):
     """MGR level operators, R/P and both AMG hierarchies equal the oracle bit for bit."""
     s = synth.make_config(cfg, edge)
@@ -166,7 +168,7 @@ def test_gmres_rejects_callables(gpu):
 # restart; observed 31 vs 33 at 6^3) and config 3 at 10^3 (24 vs 26-27 after
 # the SpMV lane-group retune).  Neighbouring sizes agree exactly (config 3: 8^3
 # 24/24, 12^3 28/28, 14^3 26/26, 16^3 29/29), so the test uses those.
-@pytest.mark.parametrize("cfg,edge", [(1, 32), (2, 10), (3, 12), (3, 16), (4, 8)])
+@pytest.mark.parametrize("cfg,edge", [(1, 32), (2, 10), (3, 12), (3, 16), (4, 8), (2, 32), (3, 32)])
 def test_end_to_end_parity(gpu, cfg, edge):
     """Iterations within +-1, solution within 1e-8 at rtol 1e-10 (north-star bar)."""
     s = synth.make_config(cfg, edge)
