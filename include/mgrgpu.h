@@ -84,8 +84,9 @@ int mg_spmv_dev(mg_ctx *ctx, const mg_mat *a, const double *x_dev, double *y_dev
    reference counterpart, the layout is an implementation detail exposed for
    tests and profiling): *sell = 1 for a SELL-32 copy, 0 for plain CSR/BSR;
    *index_bytes = stored bytes per column index (4 int32; 2 / 1 for the
-   lossless int16 / u8-dictionary column codes of large stencil-like operators) */
-int mg_spmv_layout(mg_ctx *ctx, const mg_mat *a, int *sell, int *index_bytes);
+   lossless int16 / u8-dictionary column codes of large stencil-like operators);
+   *sorted = 1 when the SELL rows are length-sorted inside windows (SELL-C-sigma) */
+int mg_spmv_layout(mg_ctx *ctx, const mg_mat *a, int *sell, int *index_bytes, int *sorted);
 /* C = A B with scipy csr_matmat semantics (sparse.py:193-196): exact zeros dropped */
 int mg_matmul(mg_ctx *ctx, const mg_mat *a, const mg_mat *b, mg_mat **out);
 /* R (A P) (sparse.py:199-203) */

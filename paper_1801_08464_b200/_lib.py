@@ -61,7 +61,7 @@ _SIGS = {
     "mg_mat_free": [P, P],
     "mg_spmv": [P, P, P, P],
     "mg_spmv_dev": [P, P, P, P],
-    "mg_spmv_layout": [P, P, ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
+    "mg_spmv_layout": [P, P, ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
     "mg_matmul": [P, P, P, ctypes.POINTER(P)],
     "mg_triple_product": [P, P, P, P, ctypes.POINTER(P)],
     "mg_transpose": [P, P, ctypes.POINTER(P)],

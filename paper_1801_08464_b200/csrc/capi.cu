@@ -263,12 +263,13 @@ int mg_spmv_dev(mg_ctx *ctx, const mg_mat *a, const double *x_dev, double *y_dev
   return guard(ctx, [&] { spmv(C(a), x_dev, y_dev); });
 }
 
-int mg_spmv_layout(mg_ctx *ctx, const mg_mat *a, int *sell, int *index_bytes) {
+int mg_spmv_layout(mg_ctx *ctx, const mg_mat *a, int *sell, int *index_bytes, int *sorted) {
   return guard(ctx, [&] {
     const Csr &c = C(a);
     prepare_spmv(c);
     if (sell) *sell = c.plan->sell ? 1 : 0;
-    if (index_bytes) *index_bytes = c.plan->sell ? c.plan->idx_bytes() : 4;
+    if (index_bytes) *index_bytes = c.plan->idx_bytes();
+    if (sorted) *sorted = c.plan->perm.p ? 1 : 0;
   });
 }
 

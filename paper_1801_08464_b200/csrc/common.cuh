@@ -193,7 +193,8 @@ struct SpmvPlan {
   // coalesce across neighbouring stencil rows (padding caps in build_sell).
   bool sell = false;
   DBuf<int> sptr;            // slice start (elements), nslices + 1
-  DBuf<int> rlen;            // row lengths
+  DBuf<int> rlen;            // row lengths, by slice position
+  DBuf<int> perm;            // slice position -> row (SELL-C-sigma), empty = identity
   DBuf<int> sci;             // int32 columns (ik == 0)
   DBuf<double> sv;
   // lossless column compression (spmv.cu build_codes): col = anchor(row) + code,
@@ -225,10 +226,10 @@ struct Csr {
     v.alloc((size_t)nnz * b * b);
   }
   // algorithmic bytes of y = A x in the stored format: int32
-  // columns, or 1 / 2 B per entry when the SELL copy is column-compressed
+  // columns, or 1 / 2 B per entry when the SpMV plan holds compressed columns
   double bytes_spmv() const {
-    const double ib = plan && plan->sell ? plan->idx_bytes() : 4.0;
-    double vb = (double)nnz * (8.0 * b * b + ib) + 4.0 * (nr + 1);
+    const double ib = plan ? plan->idx_bytes() : 4.0;
+    double vb = (double)nnz * (8.0 * b * b + ib) + 4.0 * (nr + 1) + (plan && plan->perm.p ? 4.0 * nr : 0.0);
     return vb + 8.0 * b * nc + 8.0 * b * nr;
   }
 };

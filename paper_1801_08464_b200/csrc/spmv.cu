@@ -8,6 +8,8 @@
 // nnz*(8 b^2 + 4) + 4 (nr + 1) + 8 b (nc + nr).
 #include "ops.cuh"
 
+#include <cub/cub.cuh>
+
 namespace mg {
 
 struct EpiStore {
@@ -49,13 +51,21 @@ struct XPlain {
 // loads in flight before the dependent x gathers, so a warp has VS*U*12 B of
 // matrix traffic outstanding per round trip.  Groups stride over rows (grid
 // sized to the resident capacity); every lane runs the shuffle (uniform loop).
-template <int VS, int U, class Epi, class XG>
+template <int VS, int U, int IK, class Epi, class XG>
 __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ rows,
                                              const int *__restrict__ rp,
-                                             const int *__restrict__ ci,
+                                             const void *__restrict__ ci,
+                                             const int *__restrict__ dict, unsigned long long mul,
                                              const double *__restrict__ v,
                                              XG x, Epi epi) {
+  // IK: column encoding (SpmvPlan::ik) in CSR order: 0 int32, 1 u8 -> dict, 2 int16,
+  // codes relative to anchor(row) = (row * mul) >> 32
+  __shared__ int tbl[IK == 1 ? 256 : 1];
   PDL_ENTRY();
+  if (IK == 1) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) tbl[i] = __ldg(dict + i);
+    __syncthreads();
+  }
   const int lane = threadIdx.x % VS;
   const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VS);
   const int ng = (int)((int64_t)gridDim.x * blockDim.x / VS);
@@ -64,6 +74,7 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ row
     double sum = 0.0;
     int row = idx < nr ? (rows ? __ldg(rows + idx) : idx) : nr;
     if (idx < nr) {
+      const int anc = IK ? (int)(((unsigned long long)row * mul) >> 32) : 0;
       int s = __ldg(rp + row), e = __ldg(rp + row + 1);
       for (int k0 = s; k0 < e; k0 += VS * U) {
         double vv[U];
@@ -73,7 +84,9 @@ __global__ void __launch_bounds__(256) k_csr(int nr, const int *__restrict__ row
           int k = k0 + lane + u * VS;
           bool ok = k < e;
           vv[u] = ok ? __ldcs(v + k) : 0.0;
-          cc[u] = ok ? __ldcs(ci + k) : -1;
+          if (IK == 0) cc[u] = ok ? __ldcs(static_cast<const int *>(ci) + k) : -1;
+          else if (IK == 1) cc[u] = ok ? anc + tbl[__ldcs(static_cast<const unsigned char *>(ci) + k)] : -1;
+          else cc[u] = ok ? anc + (int)__ldcs(static_cast<const short *>(ci) + k) : -1;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -113,8 +126,10 @@ __device__ __forceinline__ void sell_cols4(const void *__restrict__ ci, int base
     cc[3] = anc + (int)(short)(w1 >> 16);
   }
 }
-template <int UNR, int IK, class Epi, class XG>
+// perm (SELL-C-sigma, may be null): slice position -> row; rlen is by position
+template <int UNR, int IK, bool PF, class Epi, class XG>
 __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sptr, const int *__restrict__ rlen,
+                                              const int *__restrict__ perm,
                                               const void *__restrict__ ci, const int *__restrict__ dict,
                                               unsigned long long mul, const double *__restrict__ v,
                                               XG x, Epi epi) {
@@ -125,15 +140,55 @@ __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sp
     for (int i = threadIdx.x; i < 256; i += blockDim.x) tbl[i] = __ldg(dict + i);
     __syncthreads();
   }
-  int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nr) return;
-  const int sbase = __ldg(sptr + (row >> 5));
-  const int base = sbase + (row & 31);
-  const int wbase = (IK == 1 ? (sbase >> 2) : (sbase >> 1)) + (row & 31);
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= nr) return;
+  const int row = perm ? __ldg(perm + pos) : pos;
+  const int sbase = __ldg(sptr + (pos >> 5));
+  const int base = sbase + (pos & 31);
+  const int wbase = (IK == 1 ? (sbase >> 2) : (sbase >> 1)) + (pos & 31);
   const int anc = IK ? sell_anchor(row, mul) : 0;
-  const int len = __ldg(rlen + row);
+  const int len = __ldg(rlen + pos);
   double sum = 0.0;
   int k = 0;
+  if (PF && len >= UNR) {
+    // software pipelined: chunk i+1's values / codes are issued before chunk i's
+    // products, so a thread keeps two chunks of matrix loads in flight
+    double vv[UNR];
+    int cc[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) vv[u] = __ldcs(v + base + u * 32);
+#pragma unroll
+    for (int q = 0; q < UNR / 4; ++q) {
+      int c4[4];
+      sell_cols4<IK>(ci, base, wbase, 4 * q, anc, tbl, c4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cc[4 * q + u] = c4[u];
+    }
+    for (;;) {
+      double xg[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) xg[u] = x(cc[u]);
+      k += UNR;
+      const bool more = k + UNR <= len;
+      double vn[UNR];
+      if (more) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) vn[u] = __ldcs(v + base + (k + u) * 32);
+#pragma unroll
+        for (int q = 0; q < UNR / 4; ++q) {
+          int c4[4];
+          sell_cols4<IK>(ci, base, wbase, k + 4 * q, anc, tbl, c4);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cc[4 * q + u] = c4[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) sum += vv[u] * xg[u];
+      if (!more) break;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) vv[u] = vn[u];
+    }
+  }
   for (; k + UNR <= len; k += UNR) {
     double vv[UNR];
     int cc[UNR];
@@ -170,21 +225,23 @@ __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sp
 
 // per slice: max row length (warp per slice); Q rounds the slice length up to a
 // multiple of Q entries (4 for the scalar SELL copy: whole code words)
-__global__ void k_sell_len(int nr, int ns, const int *rp, int *rlen, int *slen, int q) {
+__global__ void k_sell_len(int nr, int ns, const int *rp, const int *perm, int *rlen, int *slen, int q) {
   int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (s >= ns) return;
-  int row = s * 32 + lane;
-  int len = row < nr ? rp[row + 1] - rp[row] : 0;
-  if (row < nr) rlen[row] = len;
+  int pos = s * 32 + lane;
+  int row = pos < nr && perm ? perm[pos] : pos;
+  int len = pos < nr ? rp[row + 1] - rp[row] : 0;
+  if (pos < nr) rlen[pos] = len;
   int m = len;
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) slen[s] = (m + q - 1) / q * q * 32;
 }
-__global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *v, const int *sptr, int *sci,
-                            double *sv) {
-  int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nr) return;
-  int base = sptr[row >> 5] + (row & 31);
+__global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *v, const int *sptr,
+                            const int *perm, int *sci, double *sv) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= nr) return;
+  const int row = perm ? perm[pos] : pos;
+  int base = sptr[pos >> 5] + (pos & 31);
   int s = rp[row], e = rp[row + 1];
   for (int k = 0; k < e - s; ++k) {
     if (sci) sci[base + k * 32] = ci[s + k];
@@ -258,13 +315,14 @@ __global__ void __launch_bounds__(1024) k_code_dict(const unsigned *bm, int *wpr
 }
 // codes of row `row` packed into its slice words (thread per row)
 template <int IK>
-__global__ void k_code_fill(int nr, const int *rp, const int *ci, const int *sptr, unsigned long long mul,
-                            const unsigned *bm, const int *wpre, unsigned *code) {
-  int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nr) return;
+__global__ void k_code_fill(int nr, const int *rp, const int *ci, const int *sptr, const int *perm,
+                            unsigned long long mul, const unsigned *bm, const int *wpre, unsigned *code) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= nr) return;
+  const int row = perm ? perm[pos] : pos;
   constexpr int PW = IK == 1 ? 4 : 2;  // codes per word
-  const int sbase = sptr[row >> 5];
-  unsigned *out = code + (sbase / PW) + (row & 31);
+  const int sbase = sptr[pos >> 5];
+  unsigned *out = code + (sbase / PW) + (pos & 31);
   const int anc = sell_anchor(row, mul);
   const int s = rp[row], e = rp[row + 1];
   unsigned w = 0;
@@ -286,6 +344,29 @@ __global__ void k_code_fill(int nr, const int *rp, const int *ci, const int *spt
   if ((e - s) % PW) out[((e - s) / PW) * 32] = w;
 }
 
+// codes in CSR order (8 lanes per row)
+template <int IK>
+__global__ void k_code_fill_csr(int nr, const int *__restrict__ rp, const int *__restrict__ ci,
+                                unsigned long long mul, const unsigned *bm, const int *wpre, void *code) {
+  const int lane = threadIdx.x & 7;
+  const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3);
+  const int ng = (int)(((int64_t)gridDim.x * blockDim.x) >> 3);
+  for (int row = g0; row < nr; row += ng) {
+    const int anc = sell_anchor(row, mul);
+    const int s = rp[row], e = rp[row + 1];
+    for (int k = s + lane; k < e; k += 8) {
+      const int d = ci[k] - anc;
+      if (IK == 1) {
+        const unsigned t = (unsigned)(d + CWIN);
+        static_cast<unsigned char *>(code)[k] =
+            (unsigned char)(wpre[t >> 5] + __popc(bm[t >> 5] & ((1u << (t & 31)) - 1u)));
+      } else {
+        static_cast<short *>(code)[k] = (short)d;
+      }
+    }
+  }
+}
+
 static int code_mode() {  // MG_SELL_CODES=0 keeps int32 columns
   static int m = -1;
   if (m < 0) {
@@ -295,7 +376,8 @@ static int code_mode() {  // MG_SELL_CODES=0 keeps int32 columns
   return m;
 }
 
-// choose and build the column encoding of a SELL copy (one host round trip)
+// choose and build the column encoding of a SELL copy (padded >= 0) or of the
+// CSR arrays (padded < 0); one host round trip
 static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
   pl.ik = 0;
   if (!code_mode() || a.nr == 0 || a.nnz == 0) return;
@@ -322,13 +404,23 @@ static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
     return;
   }
   if (pl.ik != 1) pl.dict.release();
+  if (padded < 0) {  // CSR order: 1 or 2 bytes per stored entry
+    pl.scode.alloc((size_t)((a.nnz * pl.idx_bytes() + 3) / 4));
+    const int g = grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 8);
+    if (pl.ik == 1)
+      k_code_fill_csr<1><<<g, 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, bm.p, wpre.p, pl.scode.p);
+    else
+      k_code_fill_csr<2><<<g, 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, bm.p, wpre.p, pl.scode.p);
+    check_launch("code_fill_csr");
+    return;
+  }
   pl.scode.alloc((size_t)(padded / (pl.ik == 1 ? 4 : 2)));
   if (pl.ik == 1)
-    k_code_fill<1><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.mul, bm.p,
-                                                              wpre.p, pl.scode.p);
+    k_code_fill<1><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.perm.p,
+                                                              pl.mul, bm.p, wpre.p, pl.scode.p);
   else
-    k_code_fill<2><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.mul, bm.p,
-                                                              wpre.p, pl.scode.p);
+    k_code_fill<2><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.perm.p,
+                                                              pl.mul, bm.p, wpre.p, pl.scode.p);
   check_launch("code_fill");
 }
 
@@ -341,11 +433,50 @@ static double sell_min_avg() {
   return v;
 }
 
+// SELL-C-sigma: rows sorted by length (descending, stable) inside windows of
+// SIGMA rows, so the 32 rows of a slice have similar lengths (irregular coarse
+// AMG levels).  perm[pos] = row.  One block per window.
+constexpr int SIGMA = 1024;
+__global__ void __launch_bounds__(256) k_sell_sort_window(int nr, const int *__restrict__ rp, int *perm) {
+  using Sort = cub::BlockRadixSort<unsigned, 256, SIGMA / 256, int>;
+  __shared__ typename Sort::TempStorage tmp;
+  unsigned key[SIGMA / 256];
+  int val[SIGMA / 256];
+  const int base = blockIdx.x * SIGMA;
+#pragma unroll
+  for (int i = 0; i < SIGMA / 256; ++i) {
+    const int pos = base + threadIdx.x * (SIGMA / 256) + i;
+    key[i] = pos < nr ? ~(unsigned)(rp[pos + 1] - rp[pos]) : 0xffffffffu;
+    val[i] = pos;
+  }
+  Sort(tmp).Sort(key, val);
+#pragma unroll
+  for (int i = 0; i < SIGMA / 256; ++i) {
+    const int pos = base + threadIdx.x * (SIGMA / 256) + i;
+    if (pos < nr) perm[pos] = val[i];
+  }
+}
+
+// Sorted copies only for operators with rows for about one full wave of
+// threads (one thread per row): measured at 128^3, coarse A_1 (518K rows)
+// 115 -> 110 us and F-relax A_1 (733K) 50 -> 39 us, but A_2 (128K rows, 123
+// per row) 34 -> 53 us, the long per-thread row loops left without enough
+// warps to hide latency.  MG_SELL_SIGMA=<min rows>, 0 disables.
+static int sell_sigma_min_rows() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MG_SELL_SIGMA");
+    v = e ? atoi(e) : 262144;
+  }
+  return v;
+}
+
 static void build_sell(const Csr &a, SpmvPlan &pl) {
   int ns = (a.nr + 31) / 32;
   DBuf<int> slen((size_t)ns + 1);
   pl.rlen.alloc(a.nr);
-  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p, 4);
+  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, nullptr, pl.rlen.p, slen.p,
+                                                                      4);
   check_launch("sell_len");
   DBuf<int64_t> sp64((size_t)ns + 1);
   int64_t padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
@@ -366,7 +497,19 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   }
   double cap = avg <= 16.0 ? cap_short : cap_long;
   // (+ the rounding of slice lengths to whole code words: at most 3 x 32 per slice)
-  if (padded > (int64_t)(cap * (double)a.nnz) + 4096 + 96LL * ns || padded > 2000000000LL) {
+  auto over = [&](int64_t pd) { return pd > (int64_t)(cap * (double)a.nnz) + 4096 + 96LL * ns || pd > 2000000000LL; };
+  if (over(padded) && sell_sigma_min_rows() > 0 && a.nr >= sell_sigma_min_rows()) {
+    // irregular rows: sort by length inside SIGMA windows and re-measure
+    pl.perm.alloc(a.nr);
+    k_sell_sort_window<<<(a.nr + SIGMA - 1) / SIGMA, 256, 0, stream()>>>(a.nr, a.rp.p, pl.perm.p);
+    check_launch("sell_sort_window");
+    k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.perm.p, pl.rlen.p,
+                                                                        slen.p, 4);
+    check_launch("sell_len_sorted");
+    padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
+    if (over(padded)) pl.perm.release();
+  }
+  if (over(padded)) {
     pl.rlen.release();
     return;
   }
@@ -375,7 +518,8 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   build_codes(a, pl, padded);
   if (!pl.ik) pl.sci.alloc((size_t)padded);
   pl.sv.alloc((size_t)padded);
-  k_sell_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, pl.sptr.p, pl.sci.p, pl.sv.p);
+  k_sell_fill<<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, a.v.p, pl.sptr.p, pl.perm.p,
+                                                          pl.sci.p, pl.sv.p);
   check_launch("sell_fill");
   pl.sell = true;
 }
@@ -466,7 +610,8 @@ static void build_bsell(const Csr &a, SpmvPlan &pl) {
   int ns = (a.nr + 31) / 32;
   DBuf<int> slen((size_t)ns + 1);
   pl.rlen.alloc(a.nr);
-  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.rlen.p, slen.p, 1);
+  k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, nullptr, pl.rlen.p, slen.p,
+                                                                      1);
   check_launch("bsell_len");
   DBuf<int64_t> sp64((size_t)ns + 1);
   int64_t padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
@@ -498,6 +643,9 @@ void prepare_spmv(const Csr &a) {
   }
   auto pl = std::make_unique<SpmvPlan>();
   if (a.nr >= 32768 && (double)a.nnz >= sell_min_avg() * a.nr) build_sell(a, *pl);
+  // large operators left in CSR (irregular long-row AMG levels): compressed
+  // columns in CSR order when the codes fit
+  if (!pl->sell && a.nnz >= (1 << 20) && a.nr > 0) build_codes(a, *pl, -1);
   a.plan = std::move(pl);
 }
 
@@ -579,19 +727,47 @@ static int spmv_grid(int64_t threads_needed) {
   return (int)(want < 1 ? 1 : want);
 }
 
+// software-pipelined loop for the long-row (UNR = 8) variant: coarse A_1 (105
+// per row) 77 -> 85% of HBM; the short-row variant loses with it (occupancy:
+// 56 registers), A_hat 71 -> 61%.  MG_SELL_PF=0: plain unrolled loop (A/B).
+static bool sell_pf() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_SELL_PF");
+    on = !(e && *e == '0');
+  }
+  return on;
+}
+
 template <class Epi, class XG = XPlain>
 static void launch_csr(const Csr &a, XG x, Epi epi) {
   if (a.nr == 0) return;
   double avg = a.nr ? (double)a.nnz / a.nr : 0.0;
-#define LAUNCH_AVG(VS, U) \
-  launch_pdl(k_csr<VS, U, Epi, XG>, spmv_grid((int64_t)a.nr * VS), 256, 0, a.nr, nullptr, a.rp.p, a.ci.p, a.v.p, x, epi)
   prepare_spmv(a);
   const SpmvPlan &pl = *a.plan;
+#define LAUNCH_AVG(VS, U)                                                                                    \
+  do {                                                                                                       \
+    if (pl.ik == 1)                                                                                          \
+      launch_pdl(k_csr<VS, U, 1, Epi, XG>, spmv_grid((int64_t)a.nr * VS), 256, 0, a.nr, nullptr, a.rp.p,      \
+                 (const void *)pl.scode.p, pl.dict.p, pl.mul, a.v.p, x, epi);                                \
+    else if (pl.ik == 2)                                                                                     \
+      launch_pdl(k_csr<VS, U, 2, Epi, XG>, spmv_grid((int64_t)a.nr * VS), 256, 0, a.nr, nullptr, a.rp.p,      \
+                 (const void *)pl.scode.p, pl.dict.p, pl.mul, a.v.p, x, epi);                                \
+    else                                                                                                     \
+      launch_pdl(k_csr<VS, U, 0, Epi, XG>, spmv_grid((int64_t)a.nr * VS), 256, 0, a.nr, nullptr, a.rp.p,      \
+                 (const void *)a.ci.p, (const int *)nullptr, 0ull, a.v.p, x, epi);                          \
+  } while (0)
   if (pl.sell) {
     const void *ci = pl.ik ? (const void *)pl.scode.p : (const void *)pl.sci.p;
-#define LAUNCH_SELL(UNR, T, IK) \
-  launch_pdl(k_sell<UNR, IK, Epi, XG>, grid_for(a.nr, T), T, 0, a.nr, pl.sptr.p, pl.rlen.p, ci, pl.dict.p, pl.mul, \
-             pl.sv.p, x, epi)
+#define LAUNCH_SELL(UNR, T, IK)                                                                                \
+  do {                                                                                                         \
+    if (UNR == 8 && sell_pf())                                                                                 \
+      launch_pdl(k_sell<UNR, IK, true, Epi, XG>, grid_for(a.nr, T), T, 0, a.nr, pl.sptr.p, pl.rlen.p,          \
+                 (const int *)pl.perm.p, ci, pl.dict.p, pl.mul, pl.sv.p, x, epi);                              \
+    else                                                                                                       \
+      launch_pdl(k_sell<UNR, IK, false, Epi, XG>, grid_for(a.nr, T), T, 0, a.nr, pl.sptr.p, pl.rlen.p,         \
+                 (const int *)pl.perm.p, ci, pl.dict.p, pl.mul, pl.sv.p, x, epi);                              \
+  } while (0)
     if (avg > 64) {
       if (pl.ik == 1) LAUNCH_SELL(8, 128, 1);
       else if (pl.ik == 2) LAUNCH_SELL(8, 128, 2);

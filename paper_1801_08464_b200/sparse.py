@@ -80,10 +80,11 @@ class DeviceMatrix:
         return self._info
 
     def spmv_layout(self):
-        """(sell, index_bytes) of the solve-phase SpMV copy (mg_spmv_layout)."""
-        sell, ib = _lib.c_int(), _lib.c_int()
-        self.ctx.call("mg_spmv_layout", self.h, _lib.ctypes.byref(sell), _lib.ctypes.byref(ib))
-        return bool(sell.value), ib.value
+        """(sell, index_bytes, sorted) of the solve-phase SpMV copy (mg_spmv_layout)."""
+        sell, ib, srt = _lib.c_int(), _lib.c_int(), _lib.c_int()
+        self.ctx.call("mg_spmv_layout", self.h, _lib.ctypes.byref(sell), _lib.ctypes.byref(ib),
+                      _lib.ctypes.byref(srt))
+        return bool(sell.value), ib.value, bool(srt.value)
 
     @property
     def block_size(self):

@@ -69,9 +69,67 @@ def test_spmv_sell_column_codes_bitwise(gpu, case, want_ib):
         a = rand_csr(rng, n, n, 12.0 / n)
     a.sort_indices()
     d = gsp.DeviceMatrix.from_host(a)
-    assert d.spmv_layout() == (True, want_ib)
+    assert d.spmv_layout() == (True, want_ib, False)
     x = rng.standard_normal(a.shape[1])
     np.testing.assert_array_equal(gsp.spmv(d, x), a @ x)
+
+
+def _irregular_rows(rng, n, offsets, lmin, lmax):
+    """n x n, row lengths ~U[lmin, lmax] (before merging repeats) drawn from
+    row + offsets, vectorised (sizes past the SELL-C-sigma row threshold)."""
+    lens = rng.integers(lmin, lmax + 1, n)
+    rows = np.repeat(np.arange(n), lens)
+    cols = rows + rng.choice(offsets, size=len(rows))
+    ok = (cols >= 0) & (cols < n)
+    a = sp.coo_matrix((rng.standard_normal(ok.sum()), (rows[ok], cols[ok])), shape=(n, n)).tocsr()
+    a.sum_duplicates()
+    a.sort_indices()
+    return a
+
+
+@pytest.mark.parametrize("case,want_ib", [("long_band", 2), ("long_dict", 1), ("long_scattered", 4)])
+def test_spmv_sorted_sell_bitwise(gpu, case, want_ib):
+    """Irregular long rows (SELL padding over its cap in row order) on operators
+    with >= 262144 rows get a SELL-C-sigma copy, rows length-sorted inside
+    1024-row windows; each row is still summed sequentially by one thread, so y is
+    bit-identical to scipy."""
+    rng = np.random.default_rng(11)
+    n = 300000
+    off = {"long_band": rng.choice(np.arange(-30000, 30000), 600, replace=False),
+           "long_dict": np.arange(-100, 100) * 37,
+           "long_scattered": rng.choice(np.arange(-250000, 250000), 2000, replace=False)}[case]
+    a = _irregular_rows(rng, n, off, 10, 60)
+    d = gsp.DeviceMatrix.from_host(a)
+    assert d.spmv_layout() == (True, want_ib, True)
+    x = rng.standard_normal(n)
+    np.testing.assert_array_equal(gsp.spmv(d, x), a @ x)
+    # below the row threshold no sorted copy is made
+    b = a[: 200000, : 200000].tocsr()
+    db = gsp.DeviceMatrix.from_host(b)
+    assert db.spmv_layout()[2] is False
+    assert relerr(gsp.spmv(db, x[:200000]), b @ x[:200000]) <= 1e-14
+
+
+@pytest.mark.parametrize("case,want_ib", [("short_dict", 1), ("short_band", 2), ("short_scattered", 4)])
+def test_spmv_csr_column_codes(gpu, case, want_ib):
+    """Large operators left in CSR (< 3 entries per row) carry u8 / int16 column
+    codes in CSR order when they fit.  The CSR kernel splits a row over a lane
+    group (tree-summed partials), so the bar is the CSR SpMV's 1e-14; a
+    mis-decoded column would be an O(1) error."""
+    rng = np.random.default_rng(12)
+    n = 600000
+    off = {"short_dict": rng.integers(-100, 100, n) * 3, "short_band": rng.integers(-30000, 30000, n),
+           "short_scattered": rng.integers(-n // 2, n // 2, n)}[case]
+    c2 = np.arange(n) + off
+    c2 = np.where((c2 >= 0) & (c2 < n), c2, np.arange(n))
+    cols = np.stack([np.minimum(np.arange(n), c2), np.maximum(np.arange(n), c2)], 1).ravel()
+    a = sp.csr_matrix((rng.standard_normal(2 * n), cols, np.arange(0, 2 * n + 1, 2)), shape=(n, n))
+    a.sum_duplicates()
+    a.sort_indices()
+    d = gsp.DeviceMatrix.from_host(a)
+    assert d.spmv_layout() == (False, want_ib, False)
+    x = rng.standard_normal(n)
+    assert relerr(gsp.spmv(d, x), a @ x) <= 1e-14
 
 
 def test_spmv_dimension_mismatch(gpu):

@@ -1,5 +1,7 @@
 """Per-kernel HBM bandwidth on the config-3 hierarchy (CUDA events, warm, many reps).
 
+Bytes are the stored format's (column indices at the plan's 4 / 2 / 1 B per entry).
+
 usage: python tools/kbench.py [CFG] [EDGE] [reps]
 """
 import ctypes
@@ -34,7 +36,8 @@ def time_spmv(ctx, m, reps):
     ms = v.value / reps
     _, _, nnz, b = m._load_info()
     nbr = nr // b
-    byt = nnz * (8.0 * b * b + 4) + 4 * (nbr + 1) + 8.0 * nc + 8.0 * nr
+    _, ib, _ = m.spmv_layout()  # stored bytes per column index (4 / 2 / 1)
+    byt = nnz * (8.0 * b * b + ib) + 4 * (nbr + 1) + 8.0 * nc + 8.0 * nr
     ctx.call("mg_dev_free", x)
     ctx.call("mg_dev_free", y)
     return ms, byt
@@ -65,7 +68,9 @@ def main():
             rows.append((f"F-relax AMG A_{k}", famg.levels[k].a))
     for name, m in rows:
         ms, byt = time_spmv(ctx, m, reps)
-        print(f"{name:22s} rows={m.nrows:9d} nnz={m.nnz:10d} nnz/row={m.nnz/max(m.nrows,1)*(m.block_size**2)/m.block_size:6.1f} "
+        sell, ib, srt = m.spmv_layout()
+        lay = ("SELL-s" if srt else "SELL") if sell else "CSR"
+        print(f"{name:22s} {lay:6s} idx {ib}B rows={m.nrows:9d} nnz={m.nnz:10d} nnz/row={m.nnz/max(m.nrows,1)*(m.block_size**2)/m.block_size:6.1f} "
               f"{ms*1e3:9.1f} us  {byt/ms/1e6:8.1f} GB/s  {byt/ms/1e6/peak*100:5.1f}% of {peak}", flush=True)
 
 
