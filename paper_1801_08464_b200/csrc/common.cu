@@ -167,12 +167,19 @@ Ctx::~Ctx() {
   }
 }
 
-TaskGroup::TaskGroup() : parent_(g_ctx) {}
+TaskGroup::TaskGroup() : parent_(g_ctx) {
+  Ctx *root = parent_->owner ? parent_->owner : parent_;
+  std::lock_guard<std::mutex> lk(root->amu);
+  slot_ = parent_->open_groups++;
+}
 
 TaskGroup::~TaskGroup() {
   if (!joined_) {
     try { join(); } catch (...) {}
   }
+  Ctx *root = parent_->owner ? parent_->owner : parent_;
+  std::lock_guard<std::mutex> lk(root->amu);
+  parent_->open_groups--;
 }
 
 static bool concurrent_setup() {
@@ -196,24 +203,44 @@ void TaskGroup::run(std::function<void()> fn) {
     err_.push_back(e);
     return;
   }
+  // Workers belong to the root (API) context: groups may nest (a task that
+  // starts its own group) and several groups of one root may be open at once
+  // (the MGR level tasks and the coarse AMG's).  Task k of the group opened as
+  // the slot-th open group of parent context P always runs on the worker keyed
+  // (P, slot, k): the same code path gets the same workers every setup, so each
+  // worker's home pool settles on its own needs (no pool misses in steady state).
   Ctx *p = parent_;
-  size_t k = used_.size();
-  if (k >= p->workers.size()) {
-    auto w = std::make_unique<Ctx>();
-    w->device = p->device;
-    w->num_sms = p->num_sms;
-    w->owner = p;
-    w->pool_id = (int)p->workers.size() + 1;
-    // worker streams at the lowest priority: the parent's stream carries the
-    // setup's critical path (MGR RAP, coarse AMG); worker blocks fill the gaps
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    const char *pe = getenv("MG_WORKER_PRIORITY");
-    int prio = (pe && *pe == '0') ? 0 : lo;
-    MG_CUDA(cudaStreamCreateWithPriority(&w->stream, cudaStreamNonBlocking, prio));
-    p->workers.push_back(std::move(w));
+  Ctx *root = p->owner ? p->owner : p;
+  Ctx *w = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(root->amu);
+    const std::array<int, 3> key{p->pool_id, slot_, (int)used_.size()};
+    auto it = root->worker_of.find(key);
+    if (it != root->worker_of.end()) w = it->second;
+    if (!w) {
+      auto nw = std::make_unique<Ctx>();
+      nw->device = root->device;
+      nw->num_sms = root->num_sms;
+      nw->owner = root;
+      nw->pool_id = (int)root->workers.size() + 1;
+      // worker streams at the lowest priority: the parent's stream carries the
+      // setup's critical path (MGR RAP, coarse AMG); worker blocks fill the gaps
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      const char *pe = getenv("MG_WORKER_PRIORITY");
+      int prio = (pe && *pe == '0') ? 0 : lo;
+      MG_CUDA(cudaStreamCreateWithPriority(&nw->stream, cudaStreamNonBlocking, prio));
+      w = nw.get();
+      root->worker_of[key] = w;
+      root->workers.push_back(std::move(nw));
+    }
+    if (w->busy) throw MgError(MG_ERR_CUDA, "internal: setup worker already running");
+    w->busy = true;
+    // root-stream frees up to this epoch are ordered before the worker: for a
+    // nested fork, those ordered before the parent worker's own fork
+    const int64_t e = root->epoch++;
+    w->fork_epoch = p == root ? e : p->fork_epoch;
   }
-  Ctx *w = p->workers[k].get();
   w->launches = 0;
   w->syncs = 0;
   // the worker's stream starts after everything the parent enqueued so far,
@@ -223,10 +250,6 @@ void TaskGroup::run(std::function<void()> fn) {
   MG_CUDA(cudaEventRecord(ev, p->stream));
   MG_CUDA(cudaStreamWaitEvent(w->stream, ev, 0));
   cudaEventDestroy(ev);
-  {
-    std::lock_guard<std::mutex> lk(p->amu);
-    w->fork_epoch = p->epoch++;
-  }
   used_.push_back(w);
   err_.push_back(nullptr);
   joined_ = false;
@@ -258,19 +281,28 @@ std::vector<std::exception_ptr> TaskGroup::join_errors() {
   th_.clear();
   joined_ = true;
   Ctx *p = parent_;
-  for (Ctx *w : used_) {
-    p->launches += w->launches;
-    p->syncs += w->syncs;
+  Ctx *root = p->owner ? p->owner : p;
+  bool idle = true;
+  {
+    std::lock_guard<std::mutex> lk(root->amu);
+    for (Ctx *w : used_) {
+      p->launches += w->launches;
+      p->syncs += w->syncs;
+      w->busy = false;
+    }
+    for (auto &c : root->workers) idle &= !c->busy;
   }
-  if (!used_.empty()) {
-    // worker streams are idle (each task synchronises its stream before its
-    // thread ends), so everything the parent enqueues from here on is ordered
-    // after the workers' work
-    neutralise_all(p);
+  if (!used_.empty() && idle && p == root) {
+    // no worker of the root runs any more and their streams are idle (each
+    // task synchronises its stream before its thread ends), so everything the
+    // root enqueues from here on is ordered after the workers' work.  (With a
+    // group still open elsewhere, blocks freed by these workers keep their
+    // freeing stream and are reused through a cross-stream wait.)
+    neutralise_all(root);
   }
   used_.clear();
-  std::vector<std::exception_ptr> errs;
-  errs.swap(err_);
+  std::vector<std::exception_ptr> errs(err_.begin(), err_.end());
+  err_.clear();
   return errs;
 }
 

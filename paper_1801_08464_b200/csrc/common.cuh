@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <array>
+#include <deque>
 #include <exception>
 #include <functional>
 #include <initializer_list>
@@ -81,8 +83,11 @@ struct Ctx {
   int64_t fork_epoch = 0;   // worker: parent epoch at its fork
   std::mutex amu;
   // worker contexts (own stream + scratch) for concurrent setup tasks
-  Ctx *owner = nullptr;
-  std::vector<std::unique_ptr<Ctx>> workers;
+  Ctx *owner = nullptr;      // worker: the root (API) context
+  bool busy = false;         // worker: taken by an open task (root's amu)
+  int open_groups = 0;       // TaskGroups open with this context as parent
+  std::vector<std::unique_ptr<Ctx>> workers;  // root only
+  std::map<std::array<int, 3>, Ctx *> worker_of;  // root: (parent pool, group slot, task) -> worker
   ~Ctx();
 };
 
@@ -100,9 +105,10 @@ class TaskGroup {
   std::vector<std::exception_ptr> join_errors();
  private:
   Ctx *parent_;
+  int slot_ = 0;  // ordinal among the groups open on parent_ at construction
   std::vector<std::thread> th_;
   std::vector<Ctx *> used_;
-  std::vector<std::exception_ptr> err_;
+  std::deque<std::exception_ptr> err_;  // stable element addresses: tasks write their slot
   bool joined_ = true;
 };
 

@@ -97,6 +97,17 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
   if (a.nr != a.nc) throw MgError(MG_ERR_AMG_SETUP, "AMG expects a square operator");
   auto h = std::make_unique<Amg>();
   h->opts = o;
+  // levels never move once built: the solve preparation of a finished level runs
+  // on a worker stream while this thread coarsens the next one
+  h->L.reserve((size_t)std::max(o.max_levels, 1) + 1);
+  TaskGroup tasks;  // declared after h: joined before h can be destroyed
+  auto prepare_level = [](AmgLevel &v) {
+    v.l1inv.alloc((size_t)(v.n ? v.n : 1));
+    l1_inverse(v.A, v.l1inv.p);
+    prepare_spmv(v.A);
+    prepare_spmv(v.P);
+    prepare_spmv(v.R);
+  };
   {
     AmgLevel l0;
     Csr flipped;
@@ -144,7 +155,14 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
     nxt.n = ac.nr;
     nxt.A = std::move(ac);
     h->L.push_back(std::move(nxt));
+    // level li is final (A, P, R): its SELL copies / L1 norms are independent of
+    // everything below; big levels prepare on a worker (the coarsening loop is
+    // host-round-trip bound and leaves the GPU idle between its kernels)
+    AmgLevel *lp = &h->L[li];
+    if (lp->A.nnz >= (1 << 20)) tasks.run([lp, prepare_level]() { prepare_level(*lp); });
+    else prepare_level(*lp);
   }
+  tasks.join();
   for (size_t l = 0; l < h->L.size(); ++l) {
     AmgLevel &v = h->L[l];
     size_t n = (size_t)(v.n ? v.n : 1);
@@ -152,14 +170,8 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
     v.b.alloc(n);
     v.r.alloc(n);
     v.t.alloc(n);
-    if (l + 1 < h->L.size()) {
-      v.l1inv.alloc(n);
-      l1_inverse(v.A, v.l1inv.p);
-      prepare_spmv(v.A);
-      prepare_spmv(v.P);
-      prepare_spmv(v.R);
-    }
   }
+  trace("  amg prepare joined");
   AmgLevel &last = h->L.back();
   if (last.n > std::max(o.cutoff, 200) && last.n > DENSE_LIMIT)
     throw MgError(MG_ERR_AMG_SETUP, "coarsening stalled at n=" + std::to_string(last.n) +

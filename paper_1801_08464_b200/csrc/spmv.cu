@@ -250,28 +250,22 @@ __global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *
 }
 
 // ---- column compression (SpmvPlan::ik) ------------------------------------------
-// One pass over the columns: range of code = col - anchor(row) (warp-reduced
-// atomics) and a bitmap of the codes inside [-CWIN, CWIN) (read-before-atomicOr:
-// the few distinct codes of a stencil operator are set once, then only read).
-constexpr int CWIN = 1 << 20;
-constexpr int CWORDS = (2 * CWIN) / 32;
-__global__ void k_code_stats(int nr, const int *__restrict__ rp, const int *__restrict__ ci,
-                             unsigned long long mul, unsigned *bm, int *mm) {
-  const int lane = threadIdx.x & 7;
-  const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3);
-  const int ng = (int)(((int64_t)gridDim.x * blockDim.x) >> 3);
+// code = col - anchor(row).  Columns are sorted (the C-ABI's CSR contract), so a
+// row's code range is its first and last entry: one pass over the row pointers
+// gives [lo, hi].  When hi - lo < CWIN a second pass marks the distinct codes in
+// a shared-memory bitmap per block (merged into a global one), and one block
+// ranks them: <= 256 distinct -> u8 codes through a table.
+constexpr int CWIN = 1 << 17;        // bitmap window (bits): 16 KB of shared memory
+constexpr int CWORDS = CWIN / 32;
+__global__ void k_code_range(int nr, const int *__restrict__ rp, const int *__restrict__ ci,
+                             unsigned long long mul, int *mm) {
   int lo = INT_MAX, hi = INT_MIN;
-  for (int row = g0; row < nr; row += ng) {
-    const int anc = sell_anchor(row, mul);
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nr; row += gridDim.x * blockDim.x) {
     const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
-    for (int k = s + lane; k < e; k += 8) {
-      const int d = __ldg(ci + k) - anc;
-      lo = min(lo, d);
-      hi = max(hi, d);
-      if (d >= -CWIN && d < CWIN) {
-        const unsigned t = (unsigned)(d + CWIN), bit = 1u << (t & 31);
-        if (!(__ldcg(bm + (t >> 5)) & bit)) atomicOr(bm + (t >> 5), bit);
-      }
+    if (e > s) {
+      const int anc = sell_anchor(row, mul);
+      lo = min(lo, __ldg(ci + s) - anc);
+      hi = max(hi, __ldg(ci + e - 1) - anc);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -283,14 +277,40 @@ __global__ void k_code_stats(int nr, const int *__restrict__ rp, const int *__re
     atomicMax(mm + 1, hi);
   }
 }
+// distinct codes in [lo, lo + nw * 32): block bitmap in shared memory, nonzero
+// words merged into the global bitmap
+__global__ void __launch_bounds__(256) k_code_bitmap(int nr, const int *__restrict__ rp, const int *__restrict__ ci,
+                                                     unsigned long long mul, int lo, int nw, unsigned *bm) {
+  __shared__ unsigned sb[CWORDS];
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) sb[w] = 0u;
+  __syncthreads();
+  const int lane = threadIdx.x & 7;
+  const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3);
+  const int ng = (int)(((int64_t)gridDim.x * blockDim.x) >> 3);
+  for (int row = g0; row < nr; row += ng) {
+    const int anc = sell_anchor(row, mul);
+    const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
+    for (int k = s + lane; k < e; k += 8) {
+      const unsigned t = (unsigned)(__ldg(ci + k) - anc - lo);
+      atomicOr(sb + (t >> 5), 1u << (t & 31));
+    }
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < nw; w += blockDim.x)
+    if (sb[w]) atomicOr(bm + w, sb[w]);
+}
 // per-word popcounts -> exclusive prefix (one block), the distinct count into
 // mm[2] and the code table dict[rank] = code for the first 256 codes (ascending)
-__global__ void __launch_bounds__(1024) k_code_dict(const unsigned *bm, int *wpre, int *mm, int *dict) {
+__global__ void __launch_bounds__(1024) k_code_dict(const unsigned *bm, int nw, int lo, int *wpre, int *mm,
+                                                    int *dict) {
   __shared__ int part[1024];
-  constexpr int PER = CWORDS / 1024;
+  const int per = (nw + 1023) / 1024;
   const int t = threadIdx.x;
   int c = 0;
-  for (int i = 0; i < PER; ++i) c += __popc(bm[t * PER + i]);
+  for (int i = 0; i < per; ++i) {
+    const int w = t * per + i;
+    if (w < nw) c += __popc(bm[w]);
+  }
   part[t] = c;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {
@@ -300,14 +320,15 @@ __global__ void __launch_bounds__(1024) k_code_dict(const unsigned *bm, int *wpr
     __syncthreads();
   }
   int run = part[t] - c;
-  for (int i = 0; i < PER; ++i) {
-    const int w = t * PER + i;
+  for (int i = 0; i < per; ++i) {
+    const int w = t * per + i;
+    if (w >= nw) break;
     unsigned bits = bm[w];
     wpre[w] = run;
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
-      if (run < 256) dict[run] = w * 32 + b - CWIN;
+      if (run < 256) dict[run] = lo + w * 32 + b;
       ++run;
     }
   }
@@ -316,7 +337,7 @@ __global__ void __launch_bounds__(1024) k_code_dict(const unsigned *bm, int *wpr
 // codes of row `row` packed into its slice words (thread per row)
 template <int IK>
 __global__ void k_code_fill(int nr, const int *rp, const int *ci, const int *sptr, const int *perm,
-                            unsigned long long mul, const unsigned *bm, const int *wpre, unsigned *code) {
+                            unsigned long long mul, int lo, const unsigned *bm, const int *wpre, unsigned *code) {
   const int pos = blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= nr) return;
   const int row = perm ? perm[pos] : pos;
@@ -330,7 +351,7 @@ __global__ void k_code_fill(int nr, const int *rp, const int *ci, const int *spt
     const int d = ci[s + k] - anc;
     unsigned c;
     if (IK == 1) {
-      const unsigned t = (unsigned)(d + CWIN);
+      const unsigned t = (unsigned)(d - lo);
       c = (unsigned)(wpre[t >> 5] + __popc(bm[t >> 5] & ((1u << (t & 31)) - 1u)));
     } else {
       c = (unsigned)d & 0xffffu;
@@ -347,7 +368,7 @@ __global__ void k_code_fill(int nr, const int *rp, const int *ci, const int *spt
 // codes in CSR order (8 lanes per row)
 template <int IK>
 __global__ void k_code_fill_csr(int nr, const int *__restrict__ rp, const int *__restrict__ ci,
-                                unsigned long long mul, const unsigned *bm, const int *wpre, void *code) {
+                                unsigned long long mul, int lo, const unsigned *bm, const int *wpre, void *code) {
   const int lane = threadIdx.x & 7;
   const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3);
   const int ng = (int)(((int64_t)gridDim.x * blockDim.x) >> 3);
@@ -357,7 +378,7 @@ __global__ void k_code_fill_csr(int nr, const int *__restrict__ rp, const int *_
     for (int k = s + lane; k < e; k += 8) {
       const int d = ci[k] - anc;
       if (IK == 1) {
-        const unsigned t = (unsigned)(d + CWIN);
+        const unsigned t = (unsigned)(d - lo);
         static_cast<unsigned char *>(code)[k] =
             (unsigned char)(wpre[t >> 5] + __popc(bm[t >> 5] & ((1u << (t & 31)) - 1u)));
       } else {
@@ -377,50 +398,56 @@ static int code_mode() {  // MG_SELL_CODES=0 keeps int32 columns
 }
 
 // choose and build the column encoding of a SELL copy (padded >= 0) or of the
-// CSR arrays (padded < 0); one host round trip
+// CSR arrays (padded < 0); one or two host round trips
 static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
   pl.ik = 0;
   if (!code_mode() || a.nr == 0 || a.nnz == 0) return;
   pl.mul = (unsigned long long)(((unsigned __int128)(unsigned)a.nc << 32) / (unsigned)a.nr);
-  DBuf<unsigned> bm(CWORDS);
-  DBuf<int> wpre(CWORDS), mm(3);
-  MG_CUDA(cudaMemsetAsync(bm.p, 0, CWORDS * sizeof(unsigned), stream()));
-  const int init[3] = {INT_MAX, INT_MIN, 0};
-  h2d(mm.p, init, sizeof(init));
-  pl.dict.alloc(256);
-  MG_CUDA(cudaMemsetAsync(pl.dict.p, 0, 256 * sizeof(int), stream()));
-  k_code_stats<<<grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(
-      a.nr, a.rp.p, a.ci.p, pl.mul, bm.p, mm.p);
-  check_launch("code_stats");
-  k_code_dict<<<1, 1024, 0, stream()>>>(bm.p, wpre.p, mm.p, pl.dict.p);
-  check_launch("code_dict");
+  DBuf<int> mm(3);
+  dset_i32(mm.p, {INT_MAX, INT_MIN, 0});
+  k_code_range<<<grid_for(a.nr, 256, g_ctx->num_sms * 4), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, mm.p);
+  check_launch("code_range");
   int st[3];
-  d2h(st, mm.p, sizeof(st));
-  const bool in_win = st[0] >= -CWIN && st[1] < CWIN;
-  if (in_win && st[2] <= 256) pl.ik = 1;
-  else if (st[0] >= -32768 && st[1] <= 32767) pl.ik = 2;
-  if (!pl.ik) {
-    pl.dict.release();
-    return;
+  d2h(st, mm.p, 2 * sizeof(int));
+  const int lo = st[0], hi = st[1];
+  const bool fits16 = lo >= -32768 && hi <= 32767;
+  DBuf<unsigned> bm;
+  DBuf<int> wpre;
+  if ((int64_t)hi - lo < CWIN) {
+    const int nw = (int)(((int64_t)hi - lo) / 32 + 1);
+    bm.alloc(nw);
+    wpre.alloc(nw);
+    dzero(bm.p, sizeof(unsigned) * nw);
+    pl.dict.alloc(256);
+    dzero(pl.dict.p, 256 * sizeof(int));
+    k_code_bitmap<<<grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 2), 256, 0, stream()>>>(
+        a.nr, a.rp.p, a.ci.p, pl.mul, lo, nw, bm.p);
+    check_launch("code_bitmap");
+    k_code_dict<<<1, 1024, 0, stream()>>>(bm.p, nw, lo, wpre.p, mm.p, pl.dict.p);
+    check_launch("code_dict");
+    d2h(st + 2, mm.p + 2, sizeof(int));
+    if (st[2] <= 256) pl.ik = 1;
   }
+  if (!pl.ik && fits16) pl.ik = 2;
   if (pl.ik != 1) pl.dict.release();
+  if (!pl.ik) return;
   if (padded < 0) {  // CSR order: 1 or 2 bytes per stored entry
     pl.scode.alloc((size_t)((a.nnz * pl.idx_bytes() + 3) / 4));
     const int g = grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 8);
     if (pl.ik == 1)
-      k_code_fill_csr<1><<<g, 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, bm.p, wpre.p, pl.scode.p);
+      k_code_fill_csr<1><<<g, 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, lo, bm.p, wpre.p, pl.scode.p);
     else
-      k_code_fill_csr<2><<<g, 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, bm.p, wpre.p, pl.scode.p);
+      k_code_fill_csr<2><<<g, 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, lo, bm.p, wpre.p, pl.scode.p);
     check_launch("code_fill_csr");
     return;
   }
   pl.scode.alloc((size_t)(padded / (pl.ik == 1 ? 4 : 2)));
   if (pl.ik == 1)
     k_code_fill<1><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.perm.p,
-                                                              pl.mul, bm.p, wpre.p, pl.scode.p);
+                                                              pl.mul, lo, bm.p, wpre.p, pl.scode.p);
   else
     k_code_fill<2><<<grid_for(a.nr, 256), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.sptr.p, pl.perm.p,
-                                                              pl.mul, bm.p, wpre.p, pl.scode.p);
+                                                              pl.mul, lo, bm.p, wpre.p, pl.scode.p);
   check_launch("code_fill");
 }
 
