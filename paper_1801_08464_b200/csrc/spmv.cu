@@ -451,6 +451,15 @@ static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
   check_launch("code_fill");
 }
 
+static int sell_min_rows() {  // MG_SELL_MIN_ROWS: smallest operator given a SELL copy
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MG_SELL_MIN_ROWS");
+    v = e ? atoi(e) : 32768;
+  }
+  return v;
+}
+
 static double sell_min_avg() {
   static double v = -1.0;
   if (v < 0) {
@@ -525,16 +534,24 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   double cap = avg <= 16.0 ? cap_short : cap_long;
   // (+ the rounding of slice lengths to whole code words: at most 3 x 32 per slice)
   auto over = [&](int64_t pd) { return pd > (int64_t)(cap * (double)a.nnz) + 4096 + 96LL * ns || pd > 2000000000LL; };
-  if (over(padded) && sell_sigma_min_rows() > 0 && a.nr >= sell_sigma_min_rows()) {
-    // irregular rows: sort by length inside SIGMA windows and re-measure
-    pl.perm.alloc(a.nr);
-    k_sell_sort_window<<<(a.nr + SIGMA - 1) / SIGMA, 256, 0, stream()>>>(a.nr, a.rp.p, pl.perm.p);
+  // Rows of very different lengths inside a slice (irregular AMG levels; the
+  // MGR P = [W_p; I] with its 1-entry C rows next to ~6-entry F rows) leave
+  // lanes idle for the slice's longest row: sort by length inside SIGMA windows
+  // when that is needed to pass the cap, or when it cuts the padded slots by 20%
+  const bool ragged = padded > (int64_t)(1.3 * (double)a.nnz) + 4096 + 96LL * ns;
+  if ((over(padded) || ragged) && sell_sigma_min_rows() > 0 && a.nr >= sell_sigma_min_rows()) {
+    DBuf<int> perm(a.nr), rl2(a.nr), sl2((size_t)ns + 1);
+    k_sell_sort_window<<<(a.nr + SIGMA - 1) / SIGMA, 256, 0, stream()>>>(a.nr, a.rp.p, perm.p);
     check_launch("sell_sort_window");
-    k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, pl.perm.p, pl.rlen.p,
-                                                                        slen.p, 4);
+    k_sell_len<<<grid_for((int64_t)ns * 32, 256), 256, 0, stream()>>>(a.nr, ns, a.rp.p, perm.p, rl2.p, sl2.p, 4);
     check_launch("sell_len_sorted");
-    padded = exclusive_scan_i32_to_i64(slen.p, sp64.p, ns);
-    if (over(padded)) pl.perm.release();
+    const int64_t p2 = exclusive_scan_i32_to_i64(sl2.p, sp64.p, ns);
+    if (!over(p2) && (over(padded) || (double)p2 < 0.8 * (double)padded)) {
+      pl.perm = std::move(perm);
+      pl.rlen = std::move(rl2);
+      slen = std::move(sl2);
+      padded = p2;
+    }
   }
   if (over(padded)) {
     pl.rlen.release();
@@ -669,7 +686,7 @@ void prepare_spmv(const Csr &a) {
     return;
   }
   auto pl = std::make_unique<SpmvPlan>();
-  if (a.nr >= 32768 && (double)a.nnz >= sell_min_avg() * a.nr) build_sell(a, *pl);
+  if (a.nr >= sell_min_rows() && (double)a.nnz >= sell_min_avg() * a.nr) build_sell(a, *pl);
   // large operators left in CSR (irregular long-row AMG levels): compressed
   // columns in CSR order when the codes fit
   if (!pl->sell && a.nnz >= (1 << 20) && a.nr > 0) build_codes(a, *pl, -1);
