@@ -291,8 +291,11 @@ __global__ void __launch_bounds__(256) k_code_bitmap(int nr, const int *__restri
     const int anc = sell_anchor(row, mul);
     const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
     for (int k = s + lane; k < e; k += 8) {
-      const unsigned t = (unsigned)(__ldg(ci + k) - anc - lo);
-      atomicOr(sb + (t >> 5), 1u << (t & 31));
+      const unsigned t = (unsigned)(__ldg(ci + k) - anc - lo), bit = 1u << (t & 31);
+      // a stencil operator has a few dozen codes: after their first sighting the
+      // bits are only read (a shared atomic per entry on the same few words
+      // serialises the block)
+      if (!(sb[t >> 5] & bit)) atomicOr(sb + (t >> 5), bit);
     }
   }
   __syncthreads();
@@ -420,7 +423,7 @@ static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
     dzero(bm.p, sizeof(unsigned) * nw);
     pl.dict.alloc(256);
     dzero(pl.dict.p, 256 * sizeof(int));
-    k_code_bitmap<<<grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 2), 256, 0, stream()>>>(
+    k_code_bitmap<<<grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(
         a.nr, a.rp.p, a.ci.p, pl.mul, lo, nw, bm.p);
     check_launch("code_bitmap");
     k_code_dict<<<1, 1024, 0, stream()>>>(bm.p, nw, lo, wpre.p, mm.p, pl.dict.p);
