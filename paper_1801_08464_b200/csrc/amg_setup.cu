@@ -117,6 +117,26 @@ __global__ void k_strength(int n, const int *rp, const int *ci, const double *v,
   for (RowGroup<VS> g; g.row < n; g.next()) {
     const int r = (int)g.row;
     int b = rp[r], e = rp[r + 1];
+    if (e - b <= 2 * VS) {
+      // rows of up to 2 VS entries: one load of the row into registers (the
+      // three-pass loop below re-walks it with dependent loads); same results
+      const int q0 = b + g.lane, q1 = q0 + VS;
+      const bool in0 = q0 < e, in1 = q1 < e;
+      const int c0 = in0 ? __ldg(ci + q0) : r, c1 = in1 ? __ldg(ci + q1) : r;
+      const double a0 = in0 ? __ldg(v + q0) : 0.0, a1 = in1 ? __ldg(v + q1) : 0.0;
+      const bool off0 = c0 != r, off1 = c1 != r;
+      const bool has_neg = g.any((off0 && a0 < 0.0) || (off1 && a1 < 0.0));
+      const double cand0 = (off0 && a0 < 0.0) ? -a0 : ((off0 && !has_neg) ? fabs(a0) : 0.0);
+      const double cand1 = (off1 && a1 < 0.0) ? -a1 : ((off1 && !has_neg) ? fabs(a1) : 0.0);
+      const double rmax = g.max(fmax(fmax(0.0, cand0), cand1));
+      const double thr = __dmul_rn(theta, rmax);
+      const int8_t st0 = (rmax > 0.0 && cand0 >= thr) ? 1 : 0, st1 = (rmax > 0.0 && cand1 >= thr) ? 1 : 0;
+      if (in0) s[q0] = st0;
+      if (in1) s[q1] = st1;
+      const bool has = g.any((in0 && st0) || (in1 && st1));
+      if (g.lane == 0 && has && *(volatile int *)any == 0) atomicExch(any, 1);
+      continue;
+    }
     bool neg = false;
     for (int q = b + g.lane; q < e; q += VS) neg |= (ci[q] != r) && (v[q] < 0.0);
     bool has_neg = g.any(neg);
