@@ -379,8 +379,9 @@ def main():
             traffic = json.load(f).get("dram_bytes_per_launch")
     except Exception:  # noqa: BLE001
         traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_sell<4,EpiJacobi>: L1-Jacobi sweep (SELL-32 SpMV + fused update) on "
-                                          "the coarse-AMG level-0 operator (MGR Schur complement)",
+    roofline = {"bound": "hbm", "kernel": "k_sell<4, u8 codes, EpiJacobi>: L1-Jacobi sweep (SELL-32 SpMV with "
+                                          "1-byte column codes + fused update) on the coarse-AMG level-0 "
+                                          "operator (MGR Schur complement); bytes = the stored format's",
                 "achieved": k0_gbs, "peak": hbm, "unit": "GB/s", "frac": (k0_gbs / hbm) if k0_gbs else None,
                 "traffic": traffic, "peak_kind": peak_kind, "bytes_per_launch": t.k0_bytes,
                 "avg_launch_ms": t.k0_ms / max(t.k0_calls, 1), "launches_timed": int(t.k0_calls)}
