@@ -413,8 +413,82 @@ __global__ void __launch_bounds__(RB) k_dcgs2_update(double *V, int64_t ldv, int
   block_reduce_store<1>(acc, 1, partial);
 }
 
+// Thread per element, KT basis vectors per tile: u_i and w_i are loaded once per
+// tile and each thread keeps KT independent basis loads in flight (the warp-per-
+// vector kernel above re-reads u, w from L1 per vector and keeps two loads in
+// flight).  2 KT accumulators per thread, block-reduced once at the end.
+template <int KT>
+__global__ void __launch_bounds__(256) k_mdot2x_t(const double *__restrict__ V, int64_t ldv, int K,
+                                                  const double *__restrict__ u, const double *__restrict__ w,
+                                                  int64_t n, double *partial) {
+  PDL_ENTRY();
+  __shared__ double sm[8][2 * KT];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k0 = 0; k0 < K; k0 += KT) {
+    double au[KT], aw[KT];
+#pragma unroll
+    for (int t = 0; t < KT; ++t) au[t] = aw[t] = 0.0;
+    const int kt = K - k0 < KT ? K - k0 : KT;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const double ui = __ldg(u + i), wi = __ldg(w + i);
+      double v[KT];
+#pragma unroll
+      for (int t = 0; t < KT; ++t) v[t] = t < kt ? __ldcs(V + (int64_t)(k0 + t) * ldv + i) : 0.0;
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        au[t] += v[t] * ui;
+        aw[t] += v[t] * wi;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < KT; ++t) {
+      double a = au[t], b = aw[t];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, off);
+        b += __shfl_down_sync(0xffffffffu, b, off);
+      }
+      if (lane == 0) {
+        sm[wid][t] = a;
+        sm[wid][KT + t] = b;
+      }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < 2 * KT) {
+      const int t = threadIdx.x % KT;
+      if (t < kt) {
+        double s = 0.0;
+        for (int q = 0; q < 8; ++q) s += sm[q][threadIdx.x];
+        const int k = k0 + t + (threadIdx.x >= KT ? K : 0);
+        partial[(int64_t)blockIdx.x * 2 * K + k] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+static bool mdot2x_tiled() {  // MG_MDOT2X_TILED=0: warp-per-vector kernel (A/B)
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_MDOT2X_TILED");
+    on = !(e && *e == '0');
+  }
+  return on;
+}
+
 void mdot2x(const double *V, int64_t ldv, int K, const double *u, const double *w, int64_t n, double *out_dev) {
   if (K > 32) throw MgError(MG_ERR_UNSUPPORTED, "mdot2x: at most 32 vectors");
+  if (mdot2x_tiled()) {
+    int64_t want = (n + 255) / 256;
+    int cap = g_ctx->num_sms * (K <= 8 ? 3 : 2);  // resident blocks (80 / 128 registers)
+    int nb = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+    double *part = red_scratch((size_t)nb * 64);
+    if (K <= 8) launch_pdl(k_mdot2x_t<8>, nb, 256, 0, V, ldv, K, u, w, n, part);
+    else launch_pdl(k_mdot2x_t<16>, nb, 256, 0, V, ldv, K, u, w, n, part);
+    check_launch("mdot2x");
+    reduce_finish(part, nb, 2 * K, out_dev);
+    return;
+  }
   const int nw = K < 8 ? K : 8;
   int64_t want = (n + MCH - 1) / MCH;
   int64_t cap = (int64_t)g_ctx->num_sms * 8 * (8 / nw);
