@@ -313,9 +313,17 @@ __global__ void __launch_bounds__(RB) k_combine(const double *__restrict__ V, in
   for (int k = 0; k < KM; ++k) cc[k] = k < K ? y[k] : 0.0;
   for (int64_t i = blockIdx.x * (int64_t)RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
     double t = accumulate ? u[i] : 0.0;
+    // eight basis loads issued before their products (the compiler otherwise
+    // interleaves each load with the dependent add chain: one load in flight)
 #pragma unroll
-    for (int k = 0; k < KM; ++k)
-      if (k < K) t += cc[k] * V[k * ldv + i];
+    for (int k0 = 0; k0 < KM; k0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = k0 + q < K ? __ldcs(V + (int64_t)(k0 + q) * ldv + i) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (k0 + q < K) t += cc[k0 + q] * v[q];
+    }
     u[i] = t;
   }
 }
