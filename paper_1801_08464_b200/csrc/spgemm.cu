@@ -93,7 +93,7 @@ __device__ __forceinline__ void for_products(int row, int lane, const int *__res
 
 // ---- count pass: keys only ------------------------------------------------------
 template <int T, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_spgemm_count(int nrows, const int *rows, const int *arp,
+__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_count(int nrows, const int *rows, const int *arp,
                                                            const int *aci, const int *brp, const int *bci,
                                                            int *cnt) {
   __shared__ int skeys[WPB][T];
@@ -232,7 +232,7 @@ template <int T>
 __host__ __device__ constexpr size_t fill_bytes() { return (size_t)T * 4 + (size_t)T * 8 + (size_t)T * 2 + 256; }
 
 template <int T, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_spgemm_fill(int nrows, const int *rows, const int *arp,
+__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_fill(int nrows, const int *rows, const int *arp,
                                                           const int *aci, const double *av, const int *brp,
                                                           const int *bci, const double *bv, const int64_t *base,
                                                           int *oci, double *ov, int *nz) {
