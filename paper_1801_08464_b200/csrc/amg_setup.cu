@@ -579,7 +579,7 @@ __device__ void ext_row(int i, int T, WarpTables t, int lane, const ExtArgs &A) 
 }
 
 template <int T, int WPB>
-__global__ void __launch_bounds__(WPB * 32, 1536 / (WPB * 32)) k_ext_smem(int nrows, const int *rows, ExtArgs A) {
+__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_ext_smem(int nrows, const int *rows, ExtArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpTables t = carve(smem + table_bytes(T, false) * wid, T, false);
