@@ -66,6 +66,11 @@ def main():
     for k in range(famg.nlevels):
         if famg.levels[k].a.nrows >= 10000:
             rows.append((f"F-relax AMG A_{k}", famg.levels[k].a))
+    for nm, hh in (("coarse", camg), ("F-relax", famg)):
+        for k in range(min(2, hh.nlevels - 1)):
+            pk = hh.levels[k].p
+            rows.append((f"{nm} AMG P_{k}", pk))
+            rows.append((f"{nm} AMG R_{k}", pk.transpose()))
     for name, m in rows:
         ms, byt = time_spmv(ctx, m, reps)
         sell, ib, srt = m.spmv_layout()
