@@ -238,7 +238,8 @@ typedef struct {
   double rel_tol;          /* 1e-12 */
   int max_iter;            /* 400 */
   int restart;             /* 30 */
-  int reorthogonalize;     /* 1 */
+  int reorthogonalize;     /* 1: CGS2 via DCGS2 (one-reduction, delayed); 2: classic CGS2 (krylov.py:101-107
+                              pass order); 0: single CGS pass */
   int check_every;         /* 25 */
 } mg_gmres_opts;
 
@@ -284,6 +285,10 @@ typedef struct {
   double k0_ms;
   int64_t k0_calls;
   double k0_bytes;       /* algorithmic bytes per launch */
+  /* MGR F-relaxation AMG V-cycles (phase_ms[2]): count and accumulated algorithmic
+   * bytes (Amg::cycle_bytes of each cycle run) in the last profiled solve */
+  int64_t frelax_calls;
+  double frelax_bytes;
 } mg_timing;
 int mg_get_timing(mg_ctx *ctx, mg_timing *t);
 /* CUDA-event timer on the context stream (bench timed regions) */

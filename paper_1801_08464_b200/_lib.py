@@ -45,7 +45,8 @@ class Timing(ctypes.Structure):
     _fields_ = [("setup_ms", c_double), ("solve_ms", c_double), ("spmv_ms", c_double),
                 ("spmv_calls", c_int64), ("vcycle_ms", c_double), ("vcycle_calls", c_int64),
                 ("vcycle_bytes", c_double), ("spmv_bytes", c_double), ("phase_ms", c_double * 8),
-                ("k0_ms", c_double), ("k0_calls", c_int64), ("k0_bytes", c_double)]
+                ("k0_ms", c_double), ("k0_calls", c_int64), ("k0_bytes", c_double),
+                ("frelax_calls", c_int64), ("frelax_bytes", c_double)]
 
 
 _SIGS = {
@@ -189,15 +190,29 @@ class Context:
             self.lib.mg_ctx_destroy(self.h)
             self.h = None
 
+    def __del__(self):  # objects built on a context keep a reference to it
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
+
 
 _tls = threading.local()
 
 
 def ctx(device: int | None = None) -> Context:
-    c = getattr(_tls, "ctx", None)
-    if c is None or (device is not None and c.device != device):
-        c = Context(0 if device is None else device)
-        _tls.ctx = c
+    """This thread's context for ``device`` (default: the thread's current one, else
+    device 0).  One context per (thread, device), kept for the thread's lifetime:
+    switching devices does not drop (and leak) the previous device's context."""
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device is None:
+        device = getattr(_tls, "current", 0)
+    c = ctxs.get(device)
+    if c is None or c.h is None:
+        c = ctxs[device] = Context(device)
+    _tls.current = device
     return c
 
 

@@ -49,12 +49,35 @@ void alloc_release_slabs(Ctx *c) {
   c->slab_left = 0;
 }
 
+// MG_POOL=off (sanitizer runs): every buffer is its own exact-size cudaMalloc and
+// is cudaFree'd on release, so memcheck sees accesses past a buffer's end that
+// the caching allocator's rounded blocks and slabs would absorb
+static bool pool_off() {
+  static const bool off = [] {
+    const char *e = getenv("MG_POOL");
+    return e && std::string(e) == "off";
+  }();
+  return off;
+}
+
 void *dmalloc(size_t bytes) {
   if (!bytes) return nullptr;
   Ctx *c = alloc_owner();
   Ctx *me = g_ctx;
   cudaStream_t s = me->stream;
   std::lock_guard<std::mutex> lk(c->amu);
+  if (pool_off()) {
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw MgError(MG_ERR_CUDA, std::string("device allocation of ") + std::to_string(bytes) +
+                                     " bytes failed: " + cudaGetErrorString(e));
+    }
+    c->block_size[p] = Ctx::BlkInfo{bytes, me->pool_id};
+    c->dev_bytes += (int64_t)bytes;
+    return p;
+  }
   size_t rb = round_size(bytes);
   const size_t limit = rb * 2 + ((size_t)4 << 20);
   const bool worker = me->owner != nullptr;
@@ -145,6 +168,10 @@ void dfree(void *p, size_t bytes) {
   Ctx::BlkInfo bi = it->second;
   c->block_size.erase(it);
   c->dev_bytes -= (int64_t)bi.size;
+  if (pool_off()) {
+    cudaFree(p);  // synchronises the device: no stream can still be using it
+    return;
+  }
   if ((size_t)bi.home >= c->pools.size()) c->pools.resize(bi.home + 1);
   c->pools[bi.home].emplace(bi.size, Ctx::FreeBlk{p, g_ctx->stream, c->epoch});
   c->cached_bytes += bi.size;

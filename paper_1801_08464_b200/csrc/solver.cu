@@ -37,6 +37,8 @@ void prof_reset() {
   for (double &p : g_ctx->timing.phase_ms) p = 0.0;
   g_ctx->timing.k0_ms = 0.0;
   g_ctx->timing.k0_calls = 0;
+  g_ctx->timing.frelax_calls = 0;
+  g_ctx->timing.frelax_bytes = 0.0;
 }
 static bool level_prof() {
   static int on = -1;
@@ -584,6 +586,10 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
     {
       ProfScope ps(2);
       fsolve(lv.fs, lv.Aff, lv.rF.p, lv.eF.p);
+      if (g_ctx->profiling && lv.fs.amg) {
+        g_ctx->timing.frelax_calls++;
+        g_ctx->timing.frelax_bytes += lv.fs.amg->cycle_bytes();
+      }
     }
     ProfScope ps(4);
     if (zero) {
@@ -729,13 +735,13 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
     return use_anorm && res <= o.rel_tol * (a_norm * xn + b_norm);
   };
   int mmax = std::min(o.restart, o.max_iter);
-  // DCGS2 (default with reorthogonalisation, restart <= 31); MG_GMRES_CGS2=1 keeps classic CGS2
-  static int classic = -1;
-  if (classic < 0) {
-    const char *e = getenv("MG_GMRES_CGS2");
-    classic = e && *e == '1';
-  }
-  const bool dcgs2 = o.reorth && !classic && mmax <= 31;
+  // reorth 1: DCGS2 (default, restart <= 31); 2: classic CGS2, the reference's two
+  // full projection passes in krylov.py:101-107 order; 0: one CGS pass
+  const bool dcgs2 = o.reorth == 1 && mmax <= 31;
+  static const bool trace = [] {  // MG_GMRES_TRACE=1: per-step |g| and cycle-top residuals on stderr
+    const char *e = getenv("MG_GMRES_TRACE");
+    return e && *e == '1';
+  }();
   // basis row stride padded off a power of two (K streams 32 MB apart otherwise collide)
   const int64_t ldv = ((n + 1) & ~(int64_t)1) + 1024;
   DBuf<double> V((size_t)(mmax + 1) * ldv), w(n), z(n), r(n), xt(n), u(n), t(n), proj((size_t)2 * (mmax + 1) + 8),
@@ -763,6 +769,16 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
     } else {
       vcopy(r.p, b, n);
       res = b_norm;
+    }
+    if (trace) fprintf(stderr, "[gmres] cycle top: total %d res %.17g relres %.6e\n", total, res, res / b_norm);
+    if (!std::isfinite(res)) {
+      // a NaN / Inf residual (non-finite matrix, rhs or preconditioner output)
+      // cannot recover: report non-convergence now (the reference keeps
+      // iterating on NaNs until max_iter and returns converged=False too)
+      out.iterations = total;
+      out.converged = 0;
+      out.residual_norm = res;
+      return out;
     }
     double xn = use_anorm ? nrm2(x, n) : 0.0;
     if (accepted(res, xn)) {
@@ -859,6 +875,10 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
         }
         const double a2 = sigma * sigma * uu_raw - ss;
         if (!(a2 > 0.0) || !(bt > 0.0)) {  // u_j in span(Q): breakdown
+          // the step counts like the reference's (total is incremented before
+          // its den == 0 test, krylov.py:110-119), so max_iter always ends the
+          // loop even when the breakdown repeats at j = 0
+          ++total;
           k = j;
           break;
         }
@@ -904,6 +924,7 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
           break;
         }
         bool happy = hn <= 1e-14 * std::max(res, 1.0);
+        if (trace) fprintf(stderr, "[gmres] it %d |g| %.17g hn %.17g\n", total, std::fabs(g[j + 1]), hn);
         if (std::fabs(g[j + 1]) <= tol || happy || total >= o.max_iter) break;
         if (use_anorm && o.check_every && k % o.check_every == 0) {
           assemble(k, xt.p);
@@ -959,6 +980,7 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
       g[j + 1] = -sn[j] * g[j];
       g[j] = cs[j] * g[j];
       bool happy = hn <= 1e-14 * std::max(res, 1.0);
+      if (trace) fprintf(stderr, "[gmres] it %d |g| %.17g hn %.17g\n", total, std::fabs(g[j + 1]), hn);
       if (std::fabs(g[j + 1]) <= tol || happy || total >= o.max_iter) break;
       if (use_anorm && o.check_every && k % o.check_every == 0) {
         assemble(k, xt.p);

@@ -250,22 +250,27 @@ __global__ void k_sell_fill(int nr, const int *rp, const int *ci, const double *
 }
 
 // ---- column compression (SpmvPlan::ik) ------------------------------------------
-// code = col - anchor(row).  Columns are sorted (the C-ABI's CSR contract), so a
-// row's code range is its first and last entry: one pass over the row pointers
-// gives [lo, hi].  When hi - lo < CWIN a second pass marks the distinct codes in
+// code = col - anchor(row).  One pass over every stored column gives the code
+// range [lo, hi] (min / max over all entries, so an unsorted row -- legal in
+// scipy CSR -- still gets codes inside the range and never indexes the bitmap
+// out of bounds).  When hi - lo < CWIN a second pass marks the distinct codes in
 // a shared-memory bitmap per block (merged into a global one), and one block
 // ranks them: <= 256 distinct -> u8 codes through a table.
 constexpr int CWIN = 1 << 17;        // bitmap window (bits): 16 KB of shared memory
 constexpr int CWORDS = CWIN / 32;
-__global__ void k_code_range(int nr, const int *__restrict__ rp, const int *__restrict__ ci,
-                             unsigned long long mul, int *mm) {
+__global__ void __launch_bounds__(256) k_code_range(int nr, const int *__restrict__ rp,
+                                                    const int *__restrict__ ci, unsigned long long mul, int *mm) {
   int lo = INT_MAX, hi = INT_MIN;
-  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nr; row += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 7;
+  const int g0 = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3);
+  const int ng = (int)(((int64_t)gridDim.x * blockDim.x) >> 3);
+  for (int row = g0; row < nr; row += ng) {
+    const int anc = sell_anchor(row, mul);
     const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
-    if (e > s) {
-      const int anc = sell_anchor(row, mul);
-      lo = min(lo, __ldg(ci + s) - anc);
-      hi = max(hi, __ldg(ci + e - 1) - anc);
+    for (int k = s + lane; k < e; k += 8) {
+      const int t = __ldg(ci + k) - anc;
+      lo = min(lo, t);
+      hi = max(hi, t);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -408,7 +413,8 @@ static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
   pl.mul = (unsigned long long)(((unsigned __int128)(unsigned)a.nc << 32) / (unsigned)a.nr);
   DBuf<int> mm(3);
   dset_i32(mm.p, {INT_MAX, INT_MIN, 0});
-  k_code_range<<<grid_for(a.nr, 256, g_ctx->num_sms * 4), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p, pl.mul, mm.p);
+  k_code_range<<<grid_for((int64_t)a.nr * 8, 256, g_ctx->num_sms * 8), 256, 0, stream()>>>(a.nr, a.rp.p, a.ci.p,
+                                                                                           pl.mul, mm.p);
   check_launch("code_range");
   int st[3];
   d2h(st, mm.p, 2 * sizeof(int));

@@ -28,16 +28,23 @@ class GmresOptions:
     restart: int = 30
     reorthogonalize: bool = True
     check_every: int = 25
+    # GPU-only knob (not in the reference schema): how the CGS2 of krylov.py:101-107
+    # runs.  "dcgs2": one-reduction CGS2 with delayed reorthogonalisation (two basis
+    # passes per step); "cgs2": the reference's two full projection passes.
+    orthogonalization: str = "dcgs2"
 
     def __post_init__(self):
         if self.rel_tol <= 0.0:
             raise ValueError("rel_tol must be positive")
         if self.restart < 1 or self.max_iter < 1:
             raise ValueError("restart and max_iter must be at least 1")
+        if self.orthogonalization not in ("dcgs2", "cgs2"):
+            raise ValueError(f"unknown orthogonalization {self.orthogonalization!r}")
 
     def to_c(self):
-        return _lib.GmresOpts(float(self.rel_tol), int(self.max_iter), int(self.restart),
-                              int(bool(self.reorthogonalize)), int(self.check_every or 0))
+        reorth = 0 if not self.reorthogonalize else (2 if self.orthogonalization == "cgs2" else 1)
+        return _lib.GmresOpts(float(self.rel_tol), int(self.max_iter), int(self.restart), reorth,
+                              int(self.check_every or 0))
 
 
 @dataclass

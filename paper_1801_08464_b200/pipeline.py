@@ -56,9 +56,11 @@ class SolveStats:
 class SyntheticSolver:
     """Upload once, then setup / solve on the device."""
 
-    def __init__(self, rel_tol=1e-8, restart=30, max_iter=400, amg_opts=None, rp=None, frelax=None, ctx=None):
+    def __init__(self, rel_tol=1e-8, restart=30, max_iter=400, amg_opts=None, rp=None, frelax=None, ctx=None,
+                 orthogonalization="dcgs2"):
         self.ctx = ctx or _lib.ctx()
-        self.gopts = GmresOptions(rel_tol=rel_tol, restart=restart, max_iter=max_iter)
+        self.gopts = GmresOptions(rel_tol=rel_tol, restart=restart, max_iter=max_iter,
+                                  orthogonalization=orthogonalization)
         self.amg_opts = amg_opts or default_amg_options()
         self.rp = rp
         self.frelax = frelax

@@ -146,6 +146,20 @@ def test_bsr_spmv_matches_scipy(gpu, cfg, edge):
     assert relerr(gsp.spmv(d, x), a @ x) <= 1e-14
 
 
+@pytest.mark.parametrize("cfg,edge", [(2, 32), (4, 32), (3, 40)])
+def test_bsell_spmv_matches_scipy(gpu, cfg, edge):
+    """The GMRES operator as the benchmarks run it: >= 32768 block rows take the
+    block-SELL copy (spmv.cu k_bsell<2|3>, linsolve.py:100's a @ v)."""
+    s = synth.make_config(cfg, edge)
+    a = synth.to_scalar_csr(s, "cell", drop_zeros=False)
+    d = gsp.DeviceMatrix.from_bsr(s.rowptr, s.col, s.vals)
+    assert d.spmv_layout()[0] == 1
+    rng = np.random.default_rng(cfg)
+    for _ in range(2):
+        x = rng.standard_normal(s.n)
+        assert relerr(gsp.spmv(d, x), a @ x) <= 1e-14
+
+
 def test_async_upload_pipeline(gpu):
     """mg_mat_upload_bsr_async: matrices uploaded on the copy stream while the
     context is busy equal synchronous uploads; an async upload freed before
