@@ -215,7 +215,7 @@ def _oracle_solve(cfg, edge, rtol=1e-8):
     plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
     t0 = time.perf_counter()
     res, _, tm = opipe.solve_synthetic(s, rel_tol=rtol, plan=plan, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG))
-    return {"n": s.n, "iterations": res.iterations, "converged": bool(res.converged),
+    return {"n": s.n, "iterations": res.iterations, "converged": bool(res.converged), "edge_s": f"{s.nx}x{s.ny}x{s.nz}",
             "setup_s": tm["setup_s"], "solve_s": tm["solve_s"], "total_s": time.perf_counter() - t0}
 
 
@@ -238,10 +238,11 @@ class CpuBaseline:
             return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {e}"}
         finally:
             self.pool.close()
+        edge = r.get("edge_s", self.edge)
         return {"value": r["n"] / r["total_s"], "unit": UNIT, "cores": 1, "kind": "port",
                 "same_config": True, "setup_s": round(r["setup_s"], 2), "solve_s": round(r["solve_s"], 2),
                 "iterations": r["iterations"],
-                "sample": f"one full solve of the bench system (config-{self.config} generator at {self.edge}^3, "
+                "sample": f"one full solve of the bench system (config-{self.config} generator at {edge}, "
                           f"{r['n']} DOFs, rtol 1e-8): setup {r['setup_s']:.1f}s + solve {r['solve_s']:.1f}s, "
                           f"{r['iterations']} GMRES its; oracle port (numpy/scipy + C restatement), 1 thread"}
 

@@ -248,6 +248,8 @@ typedef struct {
   int converged;
   double residual_norm;
   double rhs_norm;
+  int cycles;                  /* restart cycles run (Arnoldi loops) */
+  int first_cycle_iterations;  /* iterations when the first cycle ended (-1: none ran) */
 } mg_gmres_result;
 
 /* right-preconditioned GMRES on `a` with preconditioner `m` (NULL = none).

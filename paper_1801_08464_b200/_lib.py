@@ -14,6 +14,7 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmgrgpu.so")
+LIB_PATH_CHECKED = os.path.join(_HERE, "libmgrgpu_checked.so")
 
 c_int, c_double, c_void_p, c_int64 = ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64
 P = c_void_p
@@ -38,7 +39,7 @@ class GmresOpts(ctypes.Structure):
 
 class GmresRes(ctypes.Structure):
     _fields_ = [("iterations", c_int), ("converged", c_int), ("residual_norm", c_double),
-                ("rhs_norm", c_double)]
+                ("rhs_norm", c_double), ("cycles", c_int), ("first_cycle_iterations", c_int)]
 
 
 class Timing(ctypes.Structure):
@@ -116,9 +117,13 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load(path: str = LIB_PATH):
-    """Load libmgrgpu.so (no CUDA call is made here)."""
+def load(path: str | None = None):
+    """Load libmgrgpu.so (no CUDA call is made here).  MG_LIB=checked loads
+    libmgrgpu_checked.so instead: the same kernels built with device-side bounds
+    checks (-DMG_BOUNDS_CHECK), for test runs only."""
     global _lib
+    if path is None:
+        path = LIB_PATH_CHECKED if os.environ.get("MG_LIB") == "checked" else LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib

@@ -226,11 +226,13 @@ __global__ void k_pmis_select(int n, const int *rp, const int *ci, const int8_t 
     bool best = true;
     for (int q = rp[i]; q < rp[i + 1] && best; ++q) {
       int j = ci[q];
+      MG_DCHECK(j >= 0 && j < n);
       if (!s[q] || j == i || state[j] != UNDEC) continue;
       if (!beats(mi, i, mu[j], j)) best = false;
     }
     for (int q = trp[i]; q < trp[i + 1] && best; ++q) {
       int j = tind[q];
+      MG_DCHECK(j >= 0 && j < n);
       if (state[j] != UNDEC) continue;
       if (!beats(mi, i, mu[j], j)) best = false;
     }
@@ -246,6 +248,7 @@ __global__ void k_pmis_update(int n, const int *rp, const int *ci, const int8_t 
   if (newc[i]) { state[i] = CPT; return; }
   for (int q = rp[i]; q < rp[i + 1]; ++q) {
     int k = ci[q];
+    MG_DCHECK(k >= 0 && k < n);
     if (s[q] && k != i && (newc[k] || state[k] == CPT)) { state[i] = FPT; return; }
   }
   // termination only needs "some point is still undecided": set the flag once

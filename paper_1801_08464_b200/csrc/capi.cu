@@ -585,6 +585,8 @@ static int gmres_common(mg_ctx *ctx, const mg_mat *a, mg_mgr *m, const double *b
   res->converged = out.converged;
   res->residual_norm = out.residual_norm;
   res->rhs_norm = out.rhs_norm;
+  res->cycles = out.cycles;
+  res->first_cycle_iterations = out.first_cycle;
   return MG_OK;
 }
 

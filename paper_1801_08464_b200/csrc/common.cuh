@@ -127,6 +127,24 @@ inline cudaStream_t stream() { return g_ctx->stream; }
 // pdl_trigger() right after, so that its own successor may start launching.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Device-side checks of the checked build (libmgrgpu_checked.so, -DMG_BOUNDS_CHECK):
+// a failed check prints its site and traps, so the launch fails with
+// cudaErrorLaunchFailure and the C-ABI returns MG_ERR_CUDA.  Compiled out of
+// libmgrgpu.so.  Stand-in for compute-sanitizer, which is closed on the GPU pool.
+#ifdef MG_BOUNDS_CHECK
+#define MG_DCHECK(cond)                                                                         \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("MG_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define MG_DCHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 #define PDL_ENTRY() \
   do {              \
     pdl_wait();     \

@@ -15,7 +15,13 @@ __device__ __forceinline__ unsigned hash_k(int k, unsigned mask) {
 // insert key; returns 1 if newly inserted (keys[] initialised to -1)
 __device__ __forceinline__ int hash_insert(int *keys, unsigned mask, int k) {
   unsigned h = hash_k(k, mask);
+#ifdef MG_BOUNDS_CHECK
+  unsigned probes = 0;
+#endif
   while (true) {
+#ifdef MG_BOUNDS_CHECK
+    MG_DCHECK(probes++ <= mask);  // table full: the sizing bound was wrong
+#endif
     int cur = keys[h];
     if (cur == k) return 0;
     if (cur == -1) {
@@ -29,7 +35,15 @@ __device__ __forceinline__ int hash_insert(int *keys, unsigned mask, int k) {
 
 __device__ __forceinline__ unsigned hash_find(const int *keys, unsigned mask, int k) {
   unsigned h = hash_k(k, mask);
+#ifdef MG_BOUNDS_CHECK
+  unsigned probes = 0;
+  while (keys[h] != k) {
+    MG_DCHECK(keys[h] != -1 && probes++ <= mask);  // key absent
+    h = (h + 1) & mask;
+  }
+#else
   while (keys[h] != k) h = (h + 1) & mask;
+#endif
   return h;
 }
 
@@ -156,11 +170,13 @@ __device__ __forceinline__ void table_sort_regs(WarpTables t, int T, int u, int 
   // compact (key, slot) pairs: keys into list, slots into the (not yet used) acc area
   int *sl = (int *)t.acc;
   int filled = 0;
+  MG_DCHECK(u <= 32 * E && u <= T / 2);
   for (int i0 = 0; i0 < T; i0 += 32) {
     int k = t.keys[i0 + lane];
     unsigned bal = __ballot_sync(0xffffffffu, k != -1);
     if (k != -1) {
       int p = filled + __popc(bal & ((1u << lane) - 1));
+      MG_DCHECK(p < u);
       t.list[p] = k;
       sl[p] = i0 + lane;
     }
@@ -195,6 +211,7 @@ __device__ __forceinline__ void table_sort(WarpTables t, int T, int u, int lane)
   unsigned mask = (unsigned)T - 1;
   int P = 32;
   while (P < u) P <<= 1;
+  MG_DCHECK(P <= T / 2);  // list holds T/2 keys
   int filled = 0;
   for (int i0 = 0; i0 < T; i0 += 32) {
     int k = t.keys[i0 + lane];
@@ -202,6 +219,7 @@ __device__ __forceinline__ void table_sort(WarpTables t, int T, int u, int lane)
     if (k != -1) t.list[filled + __popc(bal & ((1u << lane) - 1))] = k;
     filled += __popc(bal);
   }
+  MG_DCHECK(filled == u);
   for (int i = u + lane; i < P; i += 32) t.list[i] = 0x7fffffff;
   __syncwarp();
   warp_bitonic(t.list, P, lane);

@@ -995,6 +995,8 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
       }
       vdiv_scalar(V.p + (int64_t)(j + 1) * ldv, w.p, hn, n);
     }
+    ++out.cycles;
+    if (out.first_cycle < 0) out.first_cycle = total;
     if (early) {
       vcopy(x, xt.p, n);
       out.iterations = total;

@@ -120,6 +120,7 @@ struct GmresOpts {
 struct GmresOut {
   int iterations = 0, converged = 0;
   double residual_norm = 0, rhs_norm = 0;
+  int cycles = 0, first_cycle = -1;  // restart cycles run; iterations when the first one ended
 };
 GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts &o, double a_norm,
                Ilu *ilu = nullptr);

@@ -26,7 +26,13 @@ namespace mg {
 // insert and return the slot; *fresh = 1 when this lane created it
 __device__ __forceinline__ int hash_insert_slot(int *keys, unsigned mask, int k, int *fresh) {
   unsigned h = hash_k(k, mask);
+#ifdef MG_BOUNDS_CHECK
+  unsigned probes = 0;
+#endif
   while (true) {
+#ifdef MG_BOUNDS_CHECK
+    MG_DCHECK(probes++ <= mask);
+#endif
     int cur = keys[h];
     if (cur == k) { *fresh = 0; return (int)h; }
     if (cur == -1) {
@@ -205,6 +211,7 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
   }
   __syncwarp();
   int64_t o = base[row];
+  MG_DCHECK(filled == u && u <= T / 2);  // list capacity; u = the count pass's size
   int nzc = 0;
   if (u <= 32) nzc = emit_sorted<1>(t, mask, u, lane, oci + o, ov + o);
   else if (u <= 64) nzc = emit_sorted<2>(t, mask, u, lane, oci + o, ov + o);
@@ -212,6 +219,7 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
   else {
     int P = 32;
     while (P < u) P <<= 1;
+    MG_DCHECK(P <= T / 2);
     for (int i = u + lane; i < P; i += 32) t.list[i] = 0x7fffffff;
     __syncwarp();
     warp_bitonic(t.list, P, lane);

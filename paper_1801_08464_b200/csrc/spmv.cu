@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(256) k_code_bitmap(int nr, const int *__restri
     const int s = __ldg(rp + row), e = __ldg(rp + row + 1);
     for (int k = s + lane; k < e; k += 8) {
       const unsigned t = (unsigned)(__ldg(ci + k) - anc - lo), bit = 1u << (t & 31);
+      MG_DCHECK(t < (unsigned)nw * 32u);
       // a stencil operator has a few dozen codes: after their first sighting the
       // bits are only read (a shared atomic per entry on the same few words
       // serialises the block)

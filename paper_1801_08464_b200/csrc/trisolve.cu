@@ -45,14 +45,21 @@ __global__ void k_trsv_lower(int n, const int *__restrict__ rp, const int *__res
       double prod = 0.0;
       if (q < e) {
         const int j = ci[q];
+        MG_DCHECK(j >= 0 && j < row);  // strictly lower: a later row would never become ready
+#ifdef MG_BOUNDS_CHECK
+        long long spins = 0;
+        while (tri_ld_acquire(ready + j) == 0) MG_DCHECK(++spins < (1LL << 32));
+#else
         while (tri_ld_acquire(ready + j) == 0) {
         }
+#endif
         prod = __dmul_rn(v[q], __ldcg(x + j));
       }
       const int cnt = min(32, e - q0);
       for (int l = 0; l < cnt; ++l) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, prod, l));
     }
     if (lane == 0) {
+      MG_DCHECK(e >= s && ci[e] == row);  // diagonal stored last
       __stcg(x + row, __ddiv_rn(acc, v[e]));
       tri_st_release(ready + row, 1);
     }

@@ -54,6 +54,8 @@ class GmresResult:
     converged: bool
     residual_norm: float
     rhs_norm: float
+    cycles: int = 0                   # GPU extra: restart cycles run
+    first_cycle_iterations: int = -1  # GPU extra: iterations when the first cycle ended
 
 
 def _as_operator(apply_a) -> DeviceMatrix:
@@ -92,4 +94,4 @@ def gmres(apply_a, apply_m, b, opts: GmresOptions = GmresOptions(), a_norm: floa
         a.ctx.call("mg_gmres", a.h, None if m is None else m.h, _lib.ptr(b), _lib.ptr(x), ctypes.byref(c),
                    -1.0 if a_norm is None else float(a_norm), ctypes.byref(res))
     return GmresResult(x, int(res.iterations), bool(res.converged), float(res.residual_norm),
-                       float(res.rhs_norm))
+                       float(res.rhs_norm), int(res.cycles), int(res.first_cycle_iterations))

@@ -35,12 +35,12 @@ def default_amg_options(**kw) -> AmgOptions:
     return AmgOptions(**d)
 
 
-def default_plan(b: int, n_cells: int, rp=None, frelax: FRelax | None = None):
+def default_plan(b: int, n_cells: int, rp=None, frelax: FRelax | None = None, global_relax=False):
     from .synth import mgr_f_indices
     if rp is None:
         rp = RpKind.NONINJECTIVE if b == 2 else RpKind.INJECTIVE
     fr = frelax or FRelax("amg", **DEFAULT_FRELAX)
-    return [(f, MgrLevelSpec((), rp, fr)) for f in mgr_f_indices(b, n_cells, order="cell")]
+    return [(f, MgrLevelSpec((), rp, fr, global_relax)) for f in mgr_f_indices(b, n_cells, order="cell")]
 
 
 @dataclass
@@ -57,13 +57,14 @@ class SyntheticSolver:
     """Upload once, then setup / solve on the device."""
 
     def __init__(self, rel_tol=1e-8, restart=30, max_iter=400, amg_opts=None, rp=None, frelax=None, ctx=None,
-                 orthogonalization="dcgs2"):
+                 orthogonalization="dcgs2", global_relax=False):
         self.ctx = ctx or _lib.ctx()
         self.gopts = GmresOptions(rel_tol=rel_tol, restart=restart, max_iter=max_iter,
                                   orthogonalization=orthogonalization)
         self.amg_opts = amg_opts or default_amg_options()
         self.rp = rp
         self.frelax = frelax
+        self.global_relax = global_relax  # per-cell block relaxation on every MGR level (mgr.py:212-251)
         self.a: DeviceMatrix | None = None
         self.hier: MgrHierarchy | None = None
         self.dinv = None
@@ -89,8 +90,10 @@ class SyntheticSolver:
         key = (b, n_cells, a.nrows)
         if self._plan is None or self._plan[0] != key:
             # the plan is an input of the setup (fixed per system shape): built once
-            self._plan = (key, compile_plan(default_plan(b, n_cells, self.rp, self.frelax), a.nrows))
-        self.hier = setup_from_matrix(self.ahat, self._plan[1], self.amg_opts)
+            self._plan = (key, compile_plan(default_plan(b, n_cells, self.rp, self.frelax, self.global_relax),
+                                            a.nrows))
+        cells = np.repeat(np.arange(n_cells, dtype=np.int64), b) if self.global_relax else None
+        self.hier = setup_from_matrix(self.ahat, self._plan[1], self.amg_opts, cells=cells)
         self.hier.set_prescale(self.dinv)
         # Ahat is copied into the hierarchy; release the standalone copy
         self.ahat.free()

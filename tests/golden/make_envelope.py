@@ -1,16 +1,22 @@
-"""Oracle self-perturbation envelopes at the BASELINE configs' stated sizes.
+"""Oracle self-perturbation envelopes (GMRES iteration counts) for the parity tests.
 
-    python tests/golden/make_envelope.py [cfg:edge:rtol ...] [--procs P]
+    python tests/golden/make_envelope.py [--procs P] [--only sweep|full]
 
 For each case the CPU oracle (oracle/pipeline.py: the reference's MGR + GMRES
-restated, PMIS / extended+i / L1 AMG) is run unperturbed and with seeds 1-4 of
-its self-perturbation ((I + 1e-15 U_a)·A and (I + 1e-13 U_m)·M^-1 with fixed random
-diagonals U, ``oracle.pipeline.gmres_synthetic``).  The iteration counts are written to
-tests/golden/envelope.json; tests/test_gpu_parity_full.py checks the GPU's count
-against [min - 1, max + 1] of this envelope at sizes too large to rerun the
-ensemble inside the GPU test step (one unperturbed oracle run is still made there
-for the solution check).  Every process is single-threaded (numpy/scipy sparse
-kernels are; BLAS pinned to 1 thread).
+restated, PMIS / extended+i / L1 AMG in the amg_mod seam) is run unperturbed and
+under its two self-perturbation models (``oracle.pipeline.gmres_synthetic``):
+"linear" (fixed random diagonal perturbations of A and M^-1) and "noise" (fresh
+per-call rounding-size noise on A·v, M^-1 and the CGS2 coefficients, calibrated
+against the measured GPU-vs-oracle differences).  Iteration counts go to
+tests/golden/envelope.json; tests/test_gpu_parity_sweep.py and
+tests/test_gpu_parity_full.py accept a GPU count in [min - 1, max + 1] of a case's
+envelope, which always contains the unperturbed oracle's count (checked again
+in the tests against an in-test oracle run).
+
+Sweep cases (config 3 edges 8..20, config 4 edges 5..12, configs 1 / 2 small):
+4 linear + 48 noise seeds.  BASELINE sizes (configs 1 / 2 at 64, config 3 at
+128^3 with rtol 1e-10 and 1e-8, config 4 at 48^3): 4 + 4 seeds (a 128^3 oracle
+solve takes ~3-4 min on one core).  Every process is single-threaded.
 """
 import json
 import multiprocessing as mp
@@ -21,12 +27,19 @@ import time
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 OUT = os.path.join(HERE, "envelope.json")
-SEEDS = (None, 1, 2, 3, 4)
-DEFAULT_CASES = ["1:64:1e-10", "2:64:1e-10", "3:128:1e-10", "3:128:1e-8"]
+
+SWEEP = ([(3, e, 1e-10) for e in range(8, 21)] + [(4, e, 1e-10) for e in range(5, 13)]
+         + [(1, 16, 1e-10), (1, 24, 1e-10), (2, 8, 1e-10), (2, 12, 1e-10), (2, 16, 1e-10)])
+FULL = [(1, 64, 1e-10), (2, 64, 1e-10), (3, 128, 1e-10), (3, 128, 1e-8), (4, 48, 1e-10)]
 
 
-def run_one(task):
-    cfg, edge, rtol, seed = task
+def key(cfg, edge, rtol):
+    return f"config{cfg}_{edge}_rtol{rtol:g}"
+
+
+def run_chunk(task):
+    """One setup, then the listed (mode, seed) solves."""
+    cfg, edge, rtol, runs = task
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
     sys.path.insert(0, ROOT)
@@ -37,38 +50,51 @@ def run_one(task):
     s = synth.make_config(cfg, edge)
     plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
     t0 = time.perf_counter()
-    state, setup_s = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=plan)
-    r = opipe.gmres_synthetic(state, s.rhs, rel_tol=rtol, perturb_seed=seed)
-    return dict(cfg=cfg, edge=edge, rtol=rtol, seed=seed, iterations=r.iterations, converged=bool(r.converged),
-                relres=r.residual_norm / r.rhs_norm, setup_s=setup_s, total_s=time.perf_counter() - t0)
+    state, _ = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=plan)
+    out = []
+    for mode, seed in runs:
+        r = opipe.gmres_synthetic(state, s.rhs, rel_tol=rtol, perturb_seed=seed, mode=mode)
+        out.append((mode, seed, r.iterations, bool(r.converged)))
+    return cfg, edge, rtol, out, time.perf_counter() - t0
+
+
+def tasks_for(cases, n_lin, n_noise, chunk):
+    runs = [("none", None)] + [("linear", s) for s in range(1, n_lin + 1)] + \
+           [("noise", 100 + s) for s in range(1, n_noise + 1)]
+    out = []
+    for cfg, edge, rtol in cases:
+        for i in range(0, len(runs), chunk):
+            out.append((cfg, edge, rtol, runs[i:i + chunk]))
+    return out
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    procs = 5
-    if "--procs" in sys.argv:
-        procs = int(sys.argv[sys.argv.index("--procs") + 1])
-        args = [a for a in args if a != str(procs)]
-    cases = args or DEFAULT_CASES
+    procs = int(sys.argv[sys.argv.index("--procs") + 1]) if "--procs" in sys.argv else max(1, (os.cpu_count() or 2) - 1)
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     tasks = []
-    for c in cases:
-        cfg, edge, rtol = c.split(":")
-        tasks += [(int(cfg), int(edge), float(rtol), sd) for sd in SEEDS]
+    if only in (None, "sweep"):
+        tasks += tasks_for(SWEEP, 4, 48, 13)
+    if only in (None, "full"):
+        tasks = tasks_for(FULL, 4, 4, 1) + tasks  # largest first
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
+    fresh = set()
     with mp.get_context("spawn").Pool(procs) as pool:
-        for r in pool.imap(run_one, tasks):
-            print(json.dumps(r), flush=True)
-            key = f"config{r['cfg']}_{r['edge']}_rtol{r['rtol']:g}"
-            e = data.setdefault(key, {"perturb": [1e-15, 1e-13], "seeds": [], "iterations": [],
-                                      "converged": []})
-            if r["seed"] in e["seeds"]:
-                k = e["seeds"].index(r["seed"])
-                e["iterations"][k], e["converged"][k] = r["iterations"], r["converged"]
-            else:
-                e["seeds"].append(r["seed"])
-                e["iterations"].append(r["iterations"])
-                e["converged"].append(r["converged"])
-            e["oracle_s"] = round(r["total_s"], 1)
+        for cfg, edge, rtol, out, el in pool.imap_unordered(run_chunk, tasks):
+            k = key(cfg, edge, rtol)
+            if k not in fresh:
+                data[k] = {"unperturbed": None, "linear": [], "noise": [], "converged": True,
+                           "models": {"linear": "oracle.pipeline.PERTURB_LINEAR (A, M^-1 relative)",
+                                      "noise": "oracle.pipeline.PERTURB_NOISE (A, M^-1, CGS2 coefficients)"}}
+                fresh.add(k)
+            e = data[k]
+            for mode, seed, its, conv in out:
+                if mode == "none":
+                    e["unperturbed"] = its
+                else:
+                    e[mode].append(its)
+                e["converged"] &= conv
+            e["oracle_s_per_chunk"] = round(el, 1)
+            print(k, out[0][0], [o[2] for o in out], f"{el:.1f}s", flush=True)
             with open(OUT, "w") as f:
                 json.dump(data, f, indent=1, sort_keys=True)
 

@@ -137,3 +137,20 @@ def test_poisson_reduction_and_cycles(gpu):
     r3 = np.linalg.norm(b - a @ gamg.amg_apply(h3, b))
     assert r3 < r1 ** 1.5
     assert 1.0 < h.operator_complexity() < 3.5
+
+
+@pytest.mark.parametrize("n_edge,cut", [(14, 3000), (16, 2000)])
+def test_large_dense_coarsest(gpu, n_edge, cut):
+    """coarse_size_cutoff in the thousands: the coarsest level is inverted by the
+    blocked Gauss-Jordan (dense.cu, n > 256) -- the V-cycle matches the oracle's
+    (scipy lu_factor at the coarsest level) within 1e-12."""
+    a = poisson3d(n_edge, 0.3)
+    kw = dict(coarse_size_cutoff=cut, pre_sweeps=2, post_sweeps=2)
+    ho = oamg.amg_setup(a, oamg.AmgOptions(**kw))
+    hg = gamg.amg_setup(a, gamg.AmgOptions(**kw))
+    assert hg.level_sizes() == ho.level_sizes() and ho.level_sizes()[-1] > 256
+    b = np.random.default_rng(3).standard_normal(a.shape[0])
+    assert relerr(gamg.amg_vcycle(hg, b), oamg.amg_vcycle(ho, b)) <= 1e-12
+    if len(ho.levels) == 1:
+        x = gamg.amg_vcycle(hg, b)
+        assert np.linalg.norm(a @ x - b) <= 1e-12 * np.linalg.norm(b) * 1e3

@@ -230,3 +230,26 @@ def test_repeated_setup_and_solve_bitwise_deterministic(gpu):
     assert r1.converged and r1.iterations == r2.iterations == r3.iterations
     np.testing.assert_array_equal(r1.x, r2.x)
     np.testing.assert_array_equal(r1.x, r3.x)
+
+
+def test_dense_inverse_needs_pivoting(gpu):
+    """IDEAL R/P and exact F / coarse solves on blocks with zero diagonals (n > 256):
+    the unpivoted blocked Gauss-Jordan rejects the pivot and the partially pivoted
+    path takes over; the apply matches the oracle (splu) within 1e-12."""
+    rng = np.random.default_rng(21)
+    nf, nc = 300, 280
+    perm = (np.arange(nf) + nf // 2) % nf
+    aff = np.zeros((nf, nf))
+    aff[np.arange(nf), perm] = 3.0 + rng.uniform(0, 1, nf)
+    aff += rng.standard_normal((nf, nf)) * 0.01 * (rng.uniform(size=(nf, nf)) < 0.02)
+    np.fill_diagonal(aff, 0.0)
+    acc = np.diag(rng.uniform(4.0, 5.0, nc)) + rng.standard_normal((nc, nc)) * 0.01
+    afc = rng.standard_normal((nf, nc)) * 0.05
+    acf = rng.standard_normal((nc, nf)) * 0.05
+    A = sp.csr_matrix(np.block([[aff, afc], [acf, acc]]))
+    f = np.arange(nf)
+    so, sg = spec_pair("ideal", "exact")
+    ho = omgr.setup_from_matrix(A, [(f, so)], coarse="exact")
+    hg = gmgr.setup_from_matrix(A, [(f, sg)], coarse="exact")
+    r = rng.standard_normal(nf + nc)
+    assert relerr(gmgr.mgr_apply(hg, r), omgr.mgr_apply(ho, r)) <= 1e-12

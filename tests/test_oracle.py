@@ -183,3 +183,29 @@ def test_oracle_pipeline_converges(cfg, edge):
     assert res.converged
     a = opipe.scalar_a(s)
     assert np.linalg.norm(s.rhs - a @ res.x) <= 1e-8 * np.linalg.norm(s.rhs) * (1 + 1e-6)
+
+
+def test_oracle_self_perturbation_moves_iterations():
+    """The explanation the GPU parity sweep leans on, shown on the oracle alone: at
+    config 3 11^3 (rtol 1e-10) rounding-size noise (oracle.pipeline PERTURB_NOISE)
+    moves the oracle's own GMRES iteration count by several iterations while the
+    solutions agree to ~1e-10; and at 10^3 the oracle's first restart is forced by
+    a rounding gap (|g| <= tol, true residual > tol)."""
+    from oracle import amg as oamg, mgr as omgr, pipeline as opipe
+    from paper_1801_08464_b200 import pipeline as gpipe, synth
+    s = synth.make_config(3, 11)
+    plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
+    state, _ = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=plan)
+    base = opipe.gmres_synthetic(state, s.rhs, rel_tol=1e-10)
+    runs = [opipe.gmres_synthetic(state, s.rhs, rel_tol=1e-10, perturb_seed=100 + k, mode="noise") for k in range(1, 9)]
+    its = [base.iterations] + [r.iterations for r in runs]
+    assert max(its) - min(its) >= 2, its
+    for r in runs:
+        assert r.converged and np.linalg.norm(r.x - base.x) <= 1e-8 * np.linalg.norm(base.x)
+    s10 = synth.make_config(3, 10)
+    state10, _ = opipe.setup_synthetic(s10, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=opipe.default_plan(
+        s10.b, s10.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX)))
+    st = {}
+    r10 = opipe.gmres_synthetic(state10, s10.rhs, rel_tol=1e-10, stats=st)
+    tol = 1e-10 * r10.rhs_norm
+    assert st["ends"][0][1] <= tol < st["tops"][1][1]

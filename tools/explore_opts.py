@@ -1,0 +1,61 @@
+"""Option exploration on one synthetic config (GPU): setup / solve ms, iterations
+and hierarchy shapes for variants of the AMG options and the MGR plan.
+
+    python tools/explore_opts.py CFG EDGE 'label:key=val,key=val' ...
+keys: any AmgOptions field (e.g. coarse_size_cutoff=2000), gr=1 (global block
+relaxation on every MGR level), frpre / frpost (F-relaxation sweeps).
+"""
+import os
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1801_08464_b200 import _lib, pipeline, synth  # noqa: E402
+from paper_1801_08464_b200.mgr import FRelax  # noqa: E402
+
+
+def run(ctx, s, label, kv, reps=3, warm=2):
+    amg_kw = dict(pipeline.DEFAULT_AMG)
+    fr_kw = dict(pipeline.DEFAULT_FRELAX)
+    gr = False
+    for k, v in kv.items():
+        if k == "gr":
+            gr = bool(int(v))
+        elif k in ("frpre", "frpost"):
+            fr_kw["pre" if k == "frpre" else "post"] = int(v)
+        else:
+            amg_kw[k] = type(pipeline.DEFAULT_AMG.get(k, 0))(v) if k in pipeline.DEFAULT_AMG else int(v)
+    solver = pipeline.SyntheticSolver(rel_tol=1e-8, ctx=ctx, amg_opts=pipeline.default_amg_options(**amg_kw),
+                                      frelax=FRelax("amg", **fr_kw), global_relax=gr)
+    solver.upload(s)
+    rows = []
+    for r in range(warm + reps):
+        solver.setup()
+        t_set = ctx.timing().setup_ms
+        res = solver.solve(s.rhs)
+        t = ctx.timing()
+        if r >= warm:
+            rows.append((t_set, t.solve_ms, res.iterations))
+    h = solver.hier
+    su = statistics.median(x[0] for x in rows)
+    so = statistics.median(x[1] for x in rows)
+    print(f"{label:28s} its {rows[-1][2]:4d} setup {su:7.1f} solve {so:7.1f} ms  {s.n / ((su + so) / 1e3) / 1e6:6.2f} "
+          f"MDOF/s  F-AMG {h.amg(0).level_sizes()} coarse {h.amg(-1).level_sizes()}", flush=True)
+    solver.hier.free()
+    solver.a.free()
+
+
+def main():
+    cfg, edge = int(sys.argv[1]), int(sys.argv[2])
+    ctx = _lib.ctx()
+    s = synth.make_config(cfg, edge)
+    for spec in sys.argv[3:]:
+        label, _, kvs = spec.partition(":")
+        kv = dict(x.split("=") for x in kvs.split(",") if x)
+        run(ctx, s, label, kv)
+
+
+if __name__ == "__main__":
+    main()
