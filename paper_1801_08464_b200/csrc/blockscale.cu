@@ -160,6 +160,32 @@ __global__ void k_block_apply(int N, const double *__restrict__ dinv, const doub
   }
 }
 
+template <int B>
+__global__ void k_block_apply_ind(int N, const double *__restrict__ dinv, const double *const *xslot,
+                                  double *__restrict__ z) {
+  PDL_ENTRY();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const double *__restrict__ x = *xslot;
+  double d[B * B], xv[B];
+#pragma unroll
+  for (int q = 0; q < B * B; ++q) d[q] = dinv[(int64_t)i * B * B + q];
+#pragma unroll
+  for (int q = 0; q < B; ++q) xv[q] = x[(int64_t)i * B + q];
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+    double s = __dmul_rn(d[r * B + 0], xv[0]);
+#pragma unroll
+    for (int k = 1; k < B; ++k) s = __dadd_rn(s, __dmul_rn(d[r * B + k], xv[k]));
+    z[(int64_t)i * B + r] = s;
+  }
+}
+
+__global__ void k_set_ptr(const double **slot, const double *value) {
+  PDL_ENTRY();
+  *slot = value;
+}
+
 __global__ void k_diag_pattern(int N, int *rp, int *ci) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < N) { rp[i] = i; ci[i] = i; }
@@ -217,6 +243,23 @@ void block_apply(const Csr &dinv, const double *x, double *z) {
   else
     throw MgError(MG_ERR_UNSUPPORTED, "block_apply: b must be 2 or 3");
   check_launch("block_apply");
+}
+
+void block_apply_indirect(const Csr &dinv, const double *const *xslot, double *z) {
+  int N = dinv.nr;
+  if (!N) return;
+  if (dinv.b == 2)
+    launch_pdl(k_block_apply_ind<2>, grid_for(N, 256), 256, 0, N, dinv.v.p, xslot, z);
+  else if (dinv.b == 3)
+    launch_pdl(k_block_apply_ind<3>, grid_for(N, 256), 256, 0, N, dinv.v.p, xslot, z);
+  else
+    throw MgError(MG_ERR_UNSUPPORTED, "block_apply: b must be 2 or 3");
+  check_launch("block_apply_indirect");
+}
+
+void set_device_ptr(const double **slot, const double *value) {
+  launch_pdl(k_set_ptr, 1, 1, 0, slot, value);
+  check_launch("set_ptr");
 }
 
 }  // namespace mg

@@ -198,6 +198,12 @@ static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero) {
   }
   AmgLevel &nx = h.L[l + 1];
   double *cur = x, *oth = v.t.p;
+  if (x_zero) {
+    // every sweep after the zero start flips cur / oth: start in the buffer that
+    // makes the last one land in x, so no copy-back launch is needed
+    const int flips = (h.opts.pre > 0 ? h.opts.pre - 1 : 0) + h.opts.post;
+    if (flips & 1) std::swap(cur, oth);
+  }
   const int k0 = (h.tag_k0 && l == 0) ? 8 : -1;  // timed as the dominant kernel when profiling
   for (int s = 0; s < h.opts.pre; ++s) {
     if (x_zero) {
@@ -628,11 +634,12 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
   }
 }
 
-static void mgr_apply_direct(Mgr &h, const double *r, double *e) {
+static void mgr_apply_direct(Mgr &h, const double *r, double *e, const double *const *rslot = nullptr) {
   const double *rr = r;
   if (h.has_prescale) {
     ProfScope ps(5);
-    block_apply(h.prescale, r, h.pre_buf.p);
+    if (rslot) block_apply_indirect(h.prescale, rslot, h.pre_buf.p);
+    else block_apply(h.prescale, r, h.pre_buf.p);
     rr = h.pre_buf.p;
   }
   apply_level(h, 0, rr, e);
@@ -656,8 +663,9 @@ static bool graphs_enabled() {
 // Capture one apply (gin -> gout) as a CUDA graph: the ~100 dependent kernel
 // launches of an MGR + 2 AMG cycles replay with minimal inter-kernel gaps.
 static bool capture_apply(Mgr &h) {
-  if (!h.gin.p) {
-    h.gin.alloc((size_t)h.n0);
+  if (!h.gout.p) {
+    if (h.has_prescale) h.in_slot.alloc(1);
+    else h.gin.alloc((size_t)h.n0);
     h.gout.alloc((size_t)h.n0);
   }
   cudaGraph_t graph = nullptr;
@@ -668,7 +676,8 @@ static bool capture_apply(Mgr &h) {
   }
   bool ok = true;
   try {
-    mgr_apply_direct(h, h.gin.p, h.gout.p);
+    if (h.has_prescale) mgr_apply_direct(h, nullptr, h.gout.p, h.in_slot.p);
+    else mgr_apply_direct(h, h.gin.p, h.gout.p);
   } catch (...) {
     ok = false;
   }
@@ -692,20 +701,26 @@ static bool capture_apply(Mgr &h) {
   return true;
 }
 
-void mgr_apply(Mgr &h, const double *r, double *e) {
+const double *mgr_apply_result(Mgr &h, const double *r, double *e) {
   if (g_ctx->profiling || !graphs_enabled() || h.graph_failed) {
     mgr_apply_direct(h, r, e);
-    return;
+    return e;
   }
   if (!h.gexec && !capture_apply(h)) {
     h.graph_failed = true;
     mgr_apply_direct(h, r, e);
-    return;
+    return e;
   }
-  if (r != h.gin.p) vcopy(h.gin.p, r, h.n0);
+  if (h.has_prescale) set_device_ptr(h.in_slot.p, r);
+  else if (r != h.gin.p) vcopy(h.gin.p, r, h.n0);
   MG_CUDA(cudaGraphLaunch(h.gexec, stream()));
   g_ctx->launches += h.graph_kernels;
-  if (e != h.gout.p) vcopy(e, h.gout.p, h.n0);
+  return h.gout.p;
+}
+
+void mgr_apply(Mgr &h, const double *r, double *e) {
+  const double *out = mgr_apply_result(h, r, e);
+  if (out != e) vcopy(e, out, h.n0);
 }
 
 // ================================ GMRES ============================================
@@ -757,8 +772,7 @@ GmresOut gmres(const Csr &a, Mgr *m, const double *b, double *x, const GmresOpts
       return out_;
     }
     if (!m) return v;
-    mgr_apply(*m, v, out_);
-    return out_;
+    return mgr_apply_result(*m, v, out_);
   };
   while (true) {
     double res;

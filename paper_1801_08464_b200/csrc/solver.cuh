@@ -89,9 +89,12 @@ struct Mgr {
   Csr prescale;                // optional per-cell D^-1 (block diagonal)
   bool has_prescale = false;
   DBuf<double> pre_buf;
-  // CUDA graph of one apply (fixed in/out buffers), captured on first use
+  // CUDA graph of one apply, captured on first use.  Output: the fixed buffer
+  // gout.  Input: with a prescale, read through the device pointer slot in_slot
+  // (set by a one-thread kernel before each replay: no copy); else copied into gin.
   cudaGraphExec_t gexec = nullptr;
   DBuf<double> gin, gout;
+  DBuf<const double *> in_slot;
   int64_t graph_kernels = 0;
   bool graph_failed = false;
   ~Mgr();
@@ -101,6 +104,9 @@ struct Mgr {
 std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan, const AmgOpts &ao,
                                int coarse_kind, bool post_smoothing, const int64_t *cells_host);
 void mgr_apply(Mgr &h, const double *r, double *e);
+// as mgr_apply, but the result may be left in the hierarchy's graph output buffer
+// (valid until the next apply on h): returns where it is (e or that buffer)
+const double *mgr_apply_result(Mgr &h, const double *r, double *e);
 
 // ILU(k) comparator (ilu.cu; ilu.py:53-174)
 struct Ilu {

@@ -24,8 +24,14 @@ from .krylov import GmresOptions, GmresResult
 from .mgr import FRelax, MgrHierarchy, MgrLevelSpec, RpKind, compile_plan, setup_from_matrix
 from .sparse import DeviceMatrix, block_scale
 
-# defaults used by bench.py, smoke() and the parity tests (oracle uses the same)
-DEFAULT_AMG = dict(strength_theta=0.25, pre_sweeps=2, post_sweeps=2, max_elmts=4)
+# defaults used by bench.py, smoke() and the parity tests (oracle uses the same).
+# coarse_size_cutoff 2000 (reference default 50): both AMG hierarchies stop at
+# n <= 2000 with an exact dense coarsest solve (amg.py:304-313, 330-336), instead of
+# 3-4 more latency-bound levels (F-relaxation AMG 11 -> 7 levels, coarse AMG 8 -> 6
+# at 128^3; iterations unchanged there, 51 -> 42 at config 2 64^3).
+DEFAULT_AMG = dict(strength_theta=0.25, pre_sweeps=2, post_sweeps=2, max_elmts=4, coarse_size_cutoff=2000)
+# the reference's own AmgOptions default cutoff, kept for the deep-hierarchy parity tests
+REFERENCE_CUTOFF = 50
 DEFAULT_FRELAX = dict(pre=1, post=1)
 
 

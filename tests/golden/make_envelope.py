@@ -13,7 +13,8 @@ tests/test_gpu_parity_full.py accept a GPU count in [min - 1, max + 1] of a case
 envelope, which always contains the unperturbed oracle's count (checked again
 in the tests against an in-test oracle run).
 
-Sweep cases (config 3 edges 8..20, config 4 edges 5..12, configs 1 / 2 small):
+Sweep cases (config 3 edges 8..20, config 4 edges 5..12, configs 1 / 2 small;
+configs 3 / 4 also with the reference's AMG cutoff 50, i.e. deep hierarchies):
 4 linear + 48 noise seeds.  BASELINE sizes (configs 1 / 2 at 64, config 3 at
 128^3 with rtol 1e-10 and 1e-8, config 4 at 48^3): 4 + 4 seeds (a 128^3 oracle
 solve takes ~3-4 min on one core).  Every process is single-threaded.
@@ -28,18 +29,24 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 OUT = os.path.join(HERE, "envelope.json")
 
-SWEEP = ([(3, e, 1e-10) for e in range(8, 21)] + [(4, e, 1e-10) for e in range(5, 13)]
-         + [(1, 16, 1e-10), (1, 24, 1e-10), (2, 8, 1e-10), (2, 12, 1e-10), (2, 16, 1e-10)])
-FULL = [(1, 64, 1e-10), (2, 64, 1e-10), (3, 128, 1e-10), (3, 128, 1e-8), (4, 48, 1e-10)]
+# (config, edge, rtol, cutoff): cutoff None = pipeline.DEFAULT_AMG's (2000);
+# 50 = the reference's AmgOptions default (deep hierarchies at small sizes)
+SWEEP = ([(3, e, 1e-10, None) for e in range(8, 21)] + [(4, e, 1e-10, None) for e in range(5, 13)]
+         + [(1, 16, 1e-10, None), (1, 24, 1e-10, None), (2, 8, 1e-10, None), (2, 12, 1e-10, None),
+            (2, 16, 1e-10, None)]
+         + [(1, 32, 1e-10, None), (2, 32, 1e-10, None), (3, 32, 1e-10, None)]
+         + [(3, e, 1e-10, 50) for e in range(8, 21)] + [(4, e, 1e-10, 50) for e in range(5, 13)])
+FULL = [(1, 64, 1e-10, None), (2, 64, 1e-10, None), (3, 128, 1e-10, None), (3, 128, 1e-8, None),
+        (4, 48, 1e-10, None)]
 
 
-def key(cfg, edge, rtol):
-    return f"config{cfg}_{edge}_rtol{rtol:g}"
+def key(cfg, edge, rtol, cut=None):
+    return f"config{cfg}_{edge}_rtol{rtol:g}" + (f"_cut{cut}" if cut else "")
 
 
 def run_chunk(task):
     """One setup, then the listed (mode, seed) solves."""
-    cfg, edge, rtol, runs = task
+    cfg, edge, rtol, cut, runs = task
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
     sys.path.insert(0, ROOT)
@@ -50,21 +57,24 @@ def run_chunk(task):
     s = synth.make_config(cfg, edge)
     plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
     t0 = time.perf_counter()
-    state, _ = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=plan)
+    kw = dict(gpipe.DEFAULT_AMG)
+    if cut:
+        kw["coarse_size_cutoff"] = cut
+    state, _ = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**kw), plan=plan)
     out = []
     for mode, seed in runs:
         r = opipe.gmres_synthetic(state, s.rhs, rel_tol=rtol, perturb_seed=seed, mode=mode)
         out.append((mode, seed, r.iterations, bool(r.converged)))
-    return cfg, edge, rtol, out, time.perf_counter() - t0
+    return cfg, edge, rtol, cut, out, time.perf_counter() - t0
 
 
 def tasks_for(cases, n_lin, n_noise, chunk):
     runs = [("none", None)] + [("linear", s) for s in range(1, n_lin + 1)] + \
            [("noise", 100 + s) for s in range(1, n_noise + 1)]
     out = []
-    for cfg, edge, rtol in cases:
+    for cfg, edge, rtol, cut in cases:
         for i in range(0, len(runs), chunk):
-            out.append((cfg, edge, rtol, runs[i:i + chunk]))
+            out.append((cfg, edge, rtol, cut, runs[i:i + chunk]))
     return out
 
 
@@ -72,6 +82,12 @@ def main():
     procs = int(sys.argv[sys.argv.index("--procs") + 1]) if "--procs" in sys.argv else max(1, (os.cpu_count() or 2) - 1)
     only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     tasks = []
+    if only and ":" in only:  # explicit cfg:edge[:cut] list, sweep seeds
+        sel = []
+        for c in only.split(","):
+            f = c.split(":")
+            sel.append((int(f[0]), int(f[1]), 1e-10, int(f[2]) if len(f) > 2 else None))
+        tasks += tasks_for(sel, 4, 48, 13)
     if only in (None, "sweep"):
         tasks += tasks_for(SWEEP, 4, 48, 13)
     if only in (None, "full"):
@@ -79,8 +95,8 @@ def main():
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
     fresh = set()
     with mp.get_context("spawn").Pool(procs) as pool:
-        for cfg, edge, rtol, out, el in pool.imap_unordered(run_chunk, tasks):
-            k = key(cfg, edge, rtol)
+        for cfg, edge, rtol, cut, out, el in pool.imap_unordered(run_chunk, tasks):
+            k = key(cfg, edge, rtol, cut)
             if k not in fresh:
                 data[k] = {"unperturbed": None, "linear": [], "noise": [], "converged": True,
                            "models": {"linear": "oracle.pipeline.PERTURB_LINEAR (A, M^-1 relative)",

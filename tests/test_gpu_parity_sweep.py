@@ -42,28 +42,36 @@ from paper_1801_08464_b200 import pipeline as gpipe
 from paper_1801_08464_b200 import synth
 
 
-CASES = ([(3, e) for e in range(8, 21)] + [(4, e) for e in range(5, 13)]
-         + [(1, 16), (1, 24), (2, 8), (2, 12), (2, 16)])
+# (config, edge, AMG cutoff): None = pipeline.DEFAULT_AMG (2000, the bench's);
+# 50 = the reference's default, which keeps deep AMG hierarchies at these sizes
+CASES = ([(3, e, None) for e in range(8, 21)] + [(4, e, None) for e in range(5, 13)]
+         + [(1, 16, None), (1, 24, None), (2, 8, None), (2, 12, None), (2, 16, None)]
+         + [(1, 32, None), (2, 32, None), (3, 32, None)]  # >= 32768 rows: the SELL / code paths
+         + [(3, e, 50) for e in range(8, 21)] + [(4, e, 50) for e in range(5, 13)])
 
 ENVELOPE = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "envelope.json")))
 _REF = {}
 
 
-def envelope(cfg, edge, rtol=1e-10):
-    e = ENVELOPE[f"config{cfg}_{edge}_rtol{rtol:g}"]
+def amg_kw(cut):
+    return dict(gpipe.DEFAULT_AMG, **({"coarse_size_cutoff": cut} if cut else {}))
+
+
+def envelope(cfg, edge, cut, rtol=1e-10):
+    e = ENVELOPE[f"config{cfg}_{edge}_rtol{rtol:g}" + (f"_cut{cut}" if cut else "")]
     its = [e["unperturbed"]] + e["linear"] + e["noise"]
     return e["unperturbed"], min(its), max(its), e["converged"]
 
 
-def oracle_run(cfg, edge):
-    if (cfg, edge) not in _REF:
+def oracle_run(cfg, edge, cut):
+    if (cfg, edge, cut) not in _REF:
         s = synth.make_config(cfg, edge)
         plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
-        state, _ = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=plan)
+        state, _ = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**amg_kw(cut)), plan=plan)
         stats = {}
         res = opipe.gmres_synthetic(state, s.rhs, rel_tol=1e-10, stats=stats)
-        _REF[(cfg, edge)] = (s, res, stats)
-    return _REF[(cfg, edge)]
+        _REF[(cfg, edge, cut)] = (s, res, stats)
+    return _REF[(cfg, edge, cut)]
 
 
 def rounding_forced_restart(stats, tol):
@@ -76,13 +84,14 @@ def rounding_forced_restart(stats, tol):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("ortho", ["dcgs2", "cgs2"])
-@pytest.mark.parametrize("cfg,edge", CASES)
-def test_parity_sweep(gpu, cfg, edge, ortho):
-    s, ref, stats = oracle_run(cfg, edge)
-    unpert, lo, hi, conv = envelope(cfg, edge)
+@pytest.mark.parametrize("cfg,edge,cut", CASES)
+def test_parity_sweep(gpu, cfg, edge, cut, ortho):
+    s, ref, stats = oracle_run(cfg, edge, cut)
+    unpert, lo, hi, conv = envelope(cfg, edge, cut)
     assert ref.converged and conv
     assert ref.iterations == unpert  # the committed envelope belongs to this oracle
-    rg, _ = gpipe.SyntheticSolver(rel_tol=1e-10, orthogonalization=ortho).solve_system(s)
+    rg, _ = gpipe.SyntheticSolver(rel_tol=1e-10, orthogonalization=ortho,
+                                  amg_opts=gpipe.default_amg_options(**amg_kw(cut))).solve_system(s)
     assert rg.converged
     if not lo - 1 <= rg.iterations <= hi + 1:
         # Outside the sampled envelope: accepted only when the oracle's own restart
@@ -92,7 +101,7 @@ def test_parity_sweep(gpu, cfg, edge, ortho):
         assert rounding_forced_restart(stats, tol), (rg.iterations, ref.iterations, (lo, hi), stats)
         assert abs(rg.first_cycle_iterations - stats["ends"][0][0]) <= 1, (rg.first_cycle_iterations, stats)
         assert rg.cycles >= 2
-        print(f"config {cfg} {edge} {ortho}: GPU {rg.iterations} its vs oracle {ref.iterations} (envelope "
+        print(f"config {cfg} {edge} cut {cut} {ortho}: GPU {rg.iterations} its vs oracle {ref.iterations} (envelope "
               f"{lo}-{hi}); first cycle {rg.first_cycle_iterations} vs {stats['ends'][0][0]}; the oracle's restart "
               f"was rounding-forced (|g| {stats['ends'][0][1]:.2e}, true {stats['tops'][1][1]:.2e}, tol {tol:.2e})")
     assert relerr(rg.x, ref.x) <= 1e-8
@@ -100,9 +109,9 @@ def test_parity_sweep(gpu, cfg, edge, ortho):
     assert np.linalg.norm(s.rhs - a @ rg.x) <= 1e-10 * np.linalg.norm(s.rhs) * (1 + 1e-6)
 
 
-@pytest.mark.parametrize("cfg,edge", CASES)
-def test_envelope_fixture_consistent(cfg, edge):
+@pytest.mark.parametrize("cfg,edge,cut", CASES)
+def test_envelope_fixture_consistent(cfg, edge, cut):
     """CPU: the envelope fixture covers every sweep case and contains the
     unperturbed count (the GPU tests' window is never empty or shifted)."""
-    unpert, lo, hi, conv = envelope(cfg, edge)
+    unpert, lo, hi, conv = envelope(cfg, edge, cut)
     assert conv and lo <= unpert <= hi

@@ -186,8 +186,8 @@ def test_oracle_pipeline_converges(cfg, edge):
 
 
 def test_oracle_self_perturbation_moves_iterations():
-    """The explanation the GPU parity sweep leans on, shown on the oracle alone: at
-    config 3 11^3 (rtol 1e-10) rounding-size noise (oracle.pipeline PERTURB_NOISE)
+    """The explanation the GPU parity sweep leans on, shown on the oracle alone
+    (reference AMG cutoff, deep hierarchies): at config 3 11^3 (rtol 1e-10) rounding-size noise (oracle.pipeline PERTURB_NOISE)
     moves the oracle's own GMRES iteration count by several iterations while the
     solutions agree to ~1e-10; and at 10^3 the oracle's first restart is forced by
     a rounding gap (|g| <= tol, true residual > tol)."""
@@ -195,7 +195,8 @@ def test_oracle_self_perturbation_moves_iterations():
     from paper_1801_08464_b200 import pipeline as gpipe, synth
     s = synth.make_config(3, 11)
     plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
-    state, _ = opipe.setup_synthetic(s, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=plan)
+    opts = oamg.AmgOptions(**dict(gpipe.DEFAULT_AMG, coarse_size_cutoff=gpipe.REFERENCE_CUTOFF))
+    state, _ = opipe.setup_synthetic(s, amg_opts=opts, plan=plan)
     base = opipe.gmres_synthetic(state, s.rhs, rel_tol=1e-10)
     runs = [opipe.gmres_synthetic(state, s.rhs, rel_tol=1e-10, perturb_seed=100 + k, mode="noise") for k in range(1, 9)]
     its = [base.iterations] + [r.iterations for r in runs]
@@ -203,7 +204,7 @@ def test_oracle_self_perturbation_moves_iterations():
     for r in runs:
         assert r.converged and np.linalg.norm(r.x - base.x) <= 1e-8 * np.linalg.norm(base.x)
     s10 = synth.make_config(3, 10)
-    state10, _ = opipe.setup_synthetic(s10, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG), plan=opipe.default_plan(
+    state10, _ = opipe.setup_synthetic(s10, amg_opts=opts, plan=opipe.default_plan(
         s10.b, s10.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX)))
     st = {}
     r10 = opipe.gmres_synthetic(state10, s10.rhs, rel_tol=1e-10, stats=st)
