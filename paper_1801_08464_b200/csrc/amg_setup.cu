@@ -194,19 +194,11 @@ __global__ void k_st_count(int n, const int *rp, const int *ci, const int8_t *s,
       if (s[q] && ci[q] != r) atomicAdd(&cnt[ci[q]], 1);
   }
 }
-template <int VS>
-__global__ void k_st_fill(int n, const int *rp, const int *ci, const int8_t *s, int *pos, int *tind) {
-  for (RowGroup<VS> g; g.row < n; g.next()) {
-    const int r = (int)g.row;
-    for (int q = rp[r] + g.lane; q < rp[r + 1]; q += VS)
-      if (s[q] && ci[q] != r) tind[atomicAdd(&pos[ci[q]], 1)] = r;
-  }
-}
-__global__ void k_pmis_init(int n, const int *trp, uint64_t seed, int level, double *mu, int8_t *state,
+__global__ void k_pmis_init(int n, const int *tcnt, uint64_t seed, int level, double *mu, int8_t *state,
                             int *undecided) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int st = trp[i + 1] - trp[i];
+  int st = tcnt[i];
   uint64_t x = seed ^ ((uint64_t)(uint32_t)level * 0x9E3779B97F4A7C15ULL) ^ (uint64_t)(int64_t)i;
   double u = __dmul_rn((double)(splitmix64(x) >> 11), 1.0 / 9007199254740992.0);
   mu[i] = __dadd_rn((double)st, u);
@@ -216,64 +208,78 @@ __global__ void k_pmis_init(int n, const int *trp, uint64_t seed, int level, dou
 __device__ __forceinline__ bool beats(double mi, int i, double mj, int j) {
   return mi > mj || (mi == mj && i > j);
 }
-__global__ void k_pmis_select(int n, const int *rp, const int *ci, const int8_t *s, const int *trp,
-                              const int *tind, const double *mu, const int8_t *state, int8_t *newc) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int8_t res = 0;
-  if (state[i] == UNDEC) {
-    double mi = mu[i];
-    bool best = true;
-    for (int q = rp[i]; q < rp[i + 1] && best; ++q) {
-      int j = ci[q];
+// One synchronous PMIS round without an explicit S^T.  The C test "mu_i beats
+// every undecided j in S_i u S^T_i" is evaluated by pushing over S only: the row
+// walk of i compares each undecided strong pair (i, j), j in S_i, and stamps the
+// loser (mark[loser] = round).  Every pair of S u S^T is some row's S entry, so
+// after the walk an undecided i is unstamped iff it beats all of them -- the same
+// set the pull formulation (S_i and S^T_i walks) selects.  Stamps of equal value
+// from several rows are benign writes; the round number makes a reset pass
+// unnecessary.
+template <int VS>
+__global__ void k_pmis_mark(int n, const int *__restrict__ rp, const int *__restrict__ ci,
+                            const int8_t *__restrict__ s, const double *__restrict__ mu,
+                            const int8_t *__restrict__ state, int *mark, int stamp) {
+  for (RowGroup<VS> g; g.row < n; g.next()) {
+    const int i = (int)g.row;
+    if (state[i] != UNDEC) continue;
+    const double mi = mu[i];
+    bool lost = false;
+    for (int q = rp[i] + g.lane; q < rp[i + 1]; q += VS) {
+      const int j = ci[q];
       MG_DCHECK(j >= 0 && j < n);
       if (!s[q] || j == i || state[j] != UNDEC) continue;
-      if (!beats(mi, i, mu[j], j)) best = false;
+      if (beats(mu[j], j, mi, i)) lost = true;
+      else mark[j] = stamp;
     }
-    for (int q = trp[i]; q < trp[i + 1] && best; ++q) {
-      int j = tind[q];
-      MG_DCHECK(j >= 0 && j < n);
-      if (state[j] != UNDEC) continue;
-      if (!beats(mi, i, mu[j], j)) best = false;
-    }
-    res = best ? 1 : 0;
+    if (g.any(lost) && g.lane == 0) mark[i] = stamp;
   }
-  newc[i] = res;
 }
-__global__ void k_pmis_update(int n, const int *rp, const int *ci, const int8_t *s, const int8_t *newc,
-                              int8_t *state, int *undecided) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (state[i] != UNDEC) return;
-  if (newc[i]) { state[i] = CPT; return; }
-  for (int q = rp[i]; q < rp[i + 1]; ++q) {
-    int k = ci[q];
-    MG_DCHECK(k >= 0 && k < n);
-    if (s[q] && k != i && (newc[k] || state[k] == CPT)) { state[i] = FPT; return; }
+// i (undecided): unstamped -> C; else F if some strong j in S_i is C (old, or new
+// this round).  The new C set is read on the fly: k is new C iff it was undecided
+// and unstamped; a k already rewritten by its own row this round reads CPT (new C)
+// or FPT (new F, never new C), so every interleaving gives the same answer.
+template <int VS>
+__global__ void k_pmis_update2(int n, const int *__restrict__ rp, const int *__restrict__ ci,
+                               const int8_t *__restrict__ s, const int *__restrict__ mark, int stamp,
+                               int8_t *state, int *undecided) {
+  for (RowGroup<VS> g; g.row < n; g.next()) {
+    const int i = (int)g.row;
+    if (state[i] != UNDEC) continue;
+    if (mark[i] != stamp) {
+      if (g.lane == 0) state[i] = CPT;
+      continue;
+    }
+    bool f = false;
+    for (int q = rp[i] + g.lane; q < rp[i + 1] && !f; q += VS) {
+      const int k = ci[q];
+      MG_DCHECK(k >= 0 && k < n);
+      if (!s[q] || k == i) continue;
+      const int8_t sk = ((volatile const int8_t *)state)[k];
+      f = sk == CPT || (sk == UNDEC && mark[k] != stamp);
+    }
+    if (g.any(f)) {
+      if (g.lane == 0) state[i] = FPT;
+    } else if (g.lane == 0 && *(volatile int *)undecided == 0) {
+      atomicExch(undecided, 1);
+    }
   }
-  // termination only needs "some point is still undecided": set the flag once
-  // (a counter incremented by every undecided row serialised the early rounds)
-  if (*(volatile int *)undecided == 0) atomicExch(undecided, 1);
 }
 
 int pmis(const Csr &a, const int8_t *s, uint64_t seed, int level, DBuf<int8_t> &state) {
   int n = a.nr;
   state.alloc((size_t)(n ? n : 1));
   if (!n) return 0;
-  DBuf<int> tcnt((size_t)n + 1), trp((size_t)n + 1), tpos((size_t)n);
+  // |S^T_i| (column counts of S) for the measure; no S^T itself
+  DBuf<int> tcnt((size_t)n + 1);
   dzero(tcnt.p, sizeof(int) * ((size_t)n + 1));
   MG_ROWGROUP_LAUNCH(k_st_count, n, a.nnz, n, a.rp.p, a.ci.p, s, tcnt.p);
   check_launch("st_count");
-  int64_t nt = exclusive_scan_i32_to_i32(tcnt.p, trp.p, n);
-  DBuf<int> tind((size_t)(nt ? nt : 1));
-  d2d(tpos.p, trp.p, sizeof(int) * (size_t)n);
-  MG_ROWGROUP_LAUNCH(k_st_fill, n, a.nnz, n, a.rp.p, a.ci.p, s, tpos.p, tind.p);
-  check_launch("st_fill");
   DBuf<double> mu(n);
-  DBuf<int8_t> newc(n);
-  DBuf<int> und(1);
+  DBuf<int> mark(n), und(1);
+  MG_CUDA(cudaMemsetAsync(mark.p, 0, sizeof(int) * (size_t)n, stream()));
   dzero(und.p, sizeof(int));
-  k_pmis_init<<<grid_for(n, 256), 256, 0, stream()>>>(n, trp.p, seed, level, mu.p, state.p, und.p);
+  k_pmis_init<<<grid_for(n, 256), 256, 0, stream()>>>(n, tcnt.p, seed, level, mu.p, state.p, und.p);
   check_launch("pmis_init");
   // rounds are checked for termination in pairs (a round with nothing
   // undecided is a no-op), halving the host round trips
@@ -282,11 +288,10 @@ int pmis(const Csr &a, const int8_t *s, uint64_t seed, int level, DBuf<int8_t> &
   while (hu > 0) {
     for (int pair = 0; pair < 2; ++pair) {
       ++rounds;
-      k_pmis_select<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, trp.p, tind.p, mu.p,
-                                                             state.p, newc.p);
-      check_launch("pmis_select");
+      MG_ROWGROUP_LAUNCH(k_pmis_mark, n, a.nnz, n, a.rp.p, a.ci.p, s, mu.p, state.p, mark.p, rounds);
+      check_launch("pmis_mark");
       dzero(und.p, sizeof(int));
-      k_pmis_update<<<grid_for(n, 256), 256, 0, stream()>>>(n, a.rp.p, a.ci.p, s, newc.p, state.p, und.p);
+      MG_ROWGROUP_LAUNCH(k_pmis_update2, n, a.nnz, n, a.rp.p, a.ci.p, s, mark.p, rounds, state.p, und.p);
       check_launch("pmis_update");
     }
     d2h(&hu, und.p, sizeof(int));

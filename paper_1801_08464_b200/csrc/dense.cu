@@ -155,38 +155,34 @@ __global__ void k_aug_extract(const double *aug, double *inv, int n) {
 // the small MGR F blocks are diagonally dominant in practice).
 constexpr int BGJ = 32;
 
-__global__ void __launch_bounds__(1024) k_bgj_diag(double *m, int n, int k0, double *dinv, int *bad) {
-  __shared__ double d[BGJ][BGJ + 1];
-  __shared__ double colk[BGJ], rowk[BGJ];
-  __shared__ double piv;
-  const int r = threadIdx.x >> 5, c = threadIdx.x & 31;
+// the diagonal block D = M_KK inverted in place by one warp: lane c holds column c
+// in registers; step k broadcasts column k (32 shuffles) and updates every column
+__global__ void __launch_bounds__(32) k_bgj_diag(double *m, int n, int k0, double *dinv, int *bad) {
+  const int c = threadIdx.x;
   const int nb = min(BGJ, n - k0);
-  d[r][c] = (r < nb && c < nb) ? m[(int64_t)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
-  __syncthreads();
+  double col[BGJ];
+#pragma unroll
+  for (int i = 0; i < BGJ; ++i)
+    col[i] = (i < nb && c < nb) ? m[(int64_t)(k0 + i) * n + k0 + c] : (i == c ? 1.0 : 0.0);
+#pragma unroll
   for (int k = 0; k < BGJ; ++k) {
-    if (threadIdx.x < 32) {  // pivot quality against the current row
-      double v = fabs(d[k][c]);
-      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (c == 0) {
-        piv = d[k][k];
-        if (!(fabs(piv) > 1e-10 * v) || !(fabs(piv) > 1e-300)) atomicCAS(bad, -1, k0 + k);
-      }
-    }
-    __syncthreads();
-    const double p = piv;
-    if (threadIdx.x < 32) { colk[c] = d[c][k]; rowk[c] = d[k][c]; }
-    __syncthreads();
+    const double rk = col[k];  // D[k][c]
+    double amax = fabs(rk);
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const double p = __shfl_sync(0xffffffffu, rk, k);
+    if (c == 0 && (!(fabs(p) > 1e-10 * amax) || !(fabs(p) > 1e-300))) atomicCAS(bad, -1, k0 + k);
     const double ip = 1.0 / p;
-    double v = d[r][c];
-    if (r == k && c == k) v = ip;
-    else if (r == k) v = rowk[c] * ip;
-    else if (c == k) v = -colk[r] * ip;
-    else v = v - colk[r] * (rowk[c] * ip);
-    __syncthreads();
-    d[r][c] = v;
-    __syncthreads();
+    const double rks = rk * ip;
+#pragma unroll
+    for (int i = 0; i < BGJ; ++i) {
+      const double ci = __shfl_sync(0xffffffffu, col[i], k);  // D[i][k]
+      if (c == k) col[i] = (i == k) ? ip : -ci * ip;
+      else if (i == k) col[i] = rks;
+      else col[i] = col[i] - ci * rks;
+    }
   }
-  dinv[r * BGJ + c] = d[r][c];
+#pragma unroll
+  for (int i = 0; i < BGJ; ++i) dinv[i * BGJ + c] = col[i];
 }
 
 // M_Kj <- D M_Kj for j outside K: one thread per column j (coalesced across j)
@@ -286,7 +282,7 @@ static int blocked_gj(const double *a_dev, double *inv_dev, int n) {
   MG_CUDA(cudaMemcpyAsync(inv_dev, a_dev, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, stream()));
   const dim3 tiles((n + 63) / 64, (n + 63) / 64);
   for (int k0 = 0; k0 < n; k0 += BGJ) {
-    k_bgj_diag<<<1, 1024, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
+    k_bgj_diag<<<1, 32, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
     k_bgj_rowpanel<<<(n + 255) / 256, 256, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
     k_bgj_update<<<tiles, 256, 0, stream()>>>(inv_dev, n, k0, bad.p);
     k_bgj_colpanel<<<(n + 255) / 256, 256, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
@@ -332,7 +328,9 @@ int dense_inverse(const double *a_dev, double *inv_dev, int n) {
   return -1;
 }
 
-// y = M x, one warp per row
+// y = M x: small n one warp per row; larger n (the coarsest levels of a few
+// thousand rows, L2-resident) four warps per row with the partial sums combined
+// in shared memory, so the grid fills the SMs.
 __global__ void k_dense_mv(const double *__restrict__ m, const double *__restrict__ x, double *y, int n) {
   PDL_ENTRY();
   int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -343,10 +341,30 @@ __global__ void k_dense_mv(const double *__restrict__ m, const double *__restric
   for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
   if (row < n && lane == 0) y[row] = s;
 }
+__global__ void __launch_bounds__(256) k_dense_mv4(const double *__restrict__ m, const double *__restrict__ x,
+                                                   double *y, int n) {
+  PDL_ENTRY();
+  __shared__ double part[8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 2 + (w >> 2), seg = w & 3;
+  double s = 0.0;
+  if (row < n) {
+    const double *mr = m + (int64_t)row * n;
+    for (int j = seg * 32 + lane; j < n; j += 128) s += mr[j] * x[j];
+  }
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  if (lane == 0) part[w] = s;
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const int r = blockIdx.x * 2 + threadIdx.x;
+    if (r < n) y[r] = (part[threadIdx.x * 4] + part[threadIdx.x * 4 + 1]) + (part[threadIdx.x * 4 + 2] + part[threadIdx.x * 4 + 3]);
+  }
+}
 
 void dense_matvec(const double *m_dev, const double *x, double *y, int n) {
   if (!n) return;
-  launch_pdl(k_dense_mv, grid_for((int64_t)n * 32, 256), 256, 0, m_dev, x, y, n);
+  if (n >= 512) launch_pdl(k_dense_mv4, (n + 1) / 2, 256, 0, m_dev, x, y, n);
+  else launch_pdl(k_dense_mv, grid_for((int64_t)n * 32, 256), 256, 0, m_dev, x, y, n);
   check_launch("dense_mv");
 }
 
