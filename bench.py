@@ -410,7 +410,7 @@ def main():
                 "achieved": k0_gbs, "peak": hbm, "unit": "GB/s", "frac": (k0_gbs / hbm) if k0_gbs else None,
                 "traffic": traffic, "peak_kind": peak_kind, "bytes_per_launch": t.k0_bytes,
                 "avg_launch_ms": t.k0_ms / max(t.k0_calls, 1), "launches_timed": int(t.k0_calls)}
-    vc_roof = {"bound": "hbm", "kernel": "coarse-grid AMG V(2,2) cycle (composite: sweeps, residual, R/P, coarsest)",
+    vc_roof = {"bound": "hbm", "kernel": "coarse-grid AMG V(1,1) cycle (composite: sweeps, residual, R/P, coarsest) -- mgr.py:369 -> amg.py:355-367",
                "achieved": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": (vc_gbs / hbm) if vc_gbs else None,
                "bytes_per_launch": t.vcycle_bytes, "avg_launch_ms": t.vcycle_ms / max(t.vcycle_calls, 1)}
     phases = {nm: round(t.phase_ms[k], 3) for k, nm in enumerate(

@@ -2,7 +2,7 @@
 
 The recommended reading of SURVEY.md §8(d) / §7 D2 in the reference API:
 
-    h = setup_from_matrix(Ahat = D^-1 A, plan, AmgOptions(pre=2, post=2))
+    h = setup_from_matrix(Ahat = D^-1 A, plan, AmgOptions(pre=1, post=1, cutoff=2000))
     gmres(lambda v: A @ v, lambda v: mgr_apply(h, Dinv @ v), b, opts)
 
 plan: b=2 [(S, NONINJECTIVE, FRelax('amg', 1, 1))];
@@ -42,7 +42,7 @@ def setup_synthetic(sysm, *, amg_opts=None, rp=None, plan=None):
     dinv, ahat = blockscale.block_scale(sysm)
     if plan is None:
         plan = default_plan(sysm.b, sysm.n_cells, rp)
-    opts = amg_opts or oamg.AmgOptions(pre_sweeps=2, post_sweeps=2)
+    opts = amg_opts or oamg.AmgOptions(coarse_size_cutoff=2000)
     hier = mgr.setup_from_matrix(CsrMatrix(ahat), plan, opts)
     return (a, dinv, hier), time.perf_counter() - t0
 

@@ -29,7 +29,12 @@ from .sparse import DeviceMatrix, block_scale
 # n <= 2000 with an exact dense coarsest solve (amg.py:304-313, 330-336), instead of
 # 3-4 more latency-bound levels (F-relaxation AMG 11 -> 7 levels, coarse AMG 8 -> 6
 # at 128^3; iterations unchanged there, 51 -> 42 at config 2 64^3).
-DEFAULT_AMG = dict(strength_theta=0.25, pre_sweeps=2, post_sweeps=2, max_elmts=4, coarse_size_cutoff=2000)
+# pre_sweeps = post_sweeps = 1: the reference's AmgOptions defaults (amg.py:36-37);
+# measured at 128^3 config 3 (tools/explore_opts.py, profiles/r02/explore_sweeps.txt):
+# V(1,1) 75 its / 134 ms solve against V(2,2) 66 its / 164 ms, and at config 4
+# 64^3 209 against 360 iterations (the L1-Jacobi V(2,2) over-smooths the non-M-matrix
+# p-Schur complement of the 3-level reduction).
+DEFAULT_AMG = dict(strength_theta=0.25, pre_sweeps=1, post_sweeps=1, max_elmts=4, coarse_size_cutoff=2000)
 # the reference's own AmgOptions default cutoff, kept for the deep-hierarchy parity tests
 REFERENCE_CUTOFF = 50
 DEFAULT_FRELAX = dict(pre=1, post=1)
