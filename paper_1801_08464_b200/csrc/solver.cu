@@ -9,6 +9,7 @@
 #include "sparse_util.cuh"
 #include "amg_kernels.cuh"
 #include "blockscale.cuh"
+#include <cub/cub.cuh>
 
 namespace mg {
 
@@ -347,13 +348,65 @@ __global__ void k_bd_gather(int nblk, const int *ioff, const int64_t *moff, cons
       o[a * k + c] = val;
     }
 }
-// small dense inverses by Gauss-Jordan with partial pivoting, one thread per block (k <= 8)
+// small dense inverses by Gauss-Jordan with partial pivoting, one thread per block
+// (k <= 8).  K > 0: the same elimination with the block size fixed at compile time,
+// so the augmented matrix lives in registers (identical operations, bitwise equal)
+template <int K>
+__device__ __forceinline__ bool bd_invert_fixed(const double *bk, double *o) {
+  double a[K][2 * K];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < 2 * K; ++j) a[i][j] = j < K ? bk[i * K + j] : (j - K == i ? 1.0 : 0.0);
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    int p = c;
+#pragma unroll
+    for (int i = c + 1; i < K; ++i)
+      if (fabs(a[i][c]) > fabs(a[p][c])) p = i;
+    // swap rows p and c with static indexing (p >= c)
+    double pr[2 * K];
+#pragma unroll
+    for (int j = 0; j < 2 * K; ++j) pr[j] = a[c][j];
+#pragma unroll
+    for (int i = c + 1; i < K; ++i)
+      if (i == p) {
+#pragma unroll
+        for (int j = 0; j < 2 * K; ++j) { double t = a[i][j]; a[i][j] = pr[j]; pr[j] = t; }
+      }
+#pragma unroll
+    for (int j = 0; j < 2 * K; ++j) a[c][j] = pr[j];
+    if (a[c][c] == 0.0) return false;
+    const double pv = a[c][c];
+#pragma unroll
+    for (int j = 0; j < 2 * K; ++j) a[c][j] /= pv;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i == c) continue;
+      const double f = a[i][c];
+      if (f != 0.0) {
+#pragma unroll
+        for (int j = 0; j < 2 * K; ++j) a[i][j] -= f * a[c][j];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) o[i * K + j] = a[i][K + j];
+  return true;
+}
 __global__ void k_bd_invert(int nblk, const int *ioff, const int64_t *moff, const double *blk, double *inv,
                             int *bad) {
   int bi = blockIdx.x * blockDim.x + threadIdx.x;
   if (bi >= nblk) return;
   const int k = ioff[bi + 1] - ioff[bi];
   const double *bk = blk + moff[bi];
+  if (k == 2 || k == 3) {
+    const bool ok = k == 2 ? bd_invert_fixed<2>(bk, inv + moff[bi]) : bd_invert_fixed<3>(bk, inv + moff[bi]);
+    if (!ok) atomicMin(bad, bi);
+    return;
+  }
   double a[8][16];
   for (int i = 0; i < k; ++i)
     for (int j = 0; j < 2 * k; ++j) a[i][j] = j < k ? bk[i * k + j] : (j - k == i ? 1.0 : 0.0);
@@ -378,53 +431,93 @@ __global__ void k_bd_invert(int nblk, const int *ioff, const int64_t *moff, cons
     for (int j = 0; j < k; ++j) o[i * k + j] = a[i][k + j];
 }
 
-static std::unique_ptr<BlockDiag> blockdiag_setup(const Csr &a, const std::vector<int64_t> &cells) {
-  // group unknowns by owning cell (stable sort of cells, mgr.py:219-224);
-  // each group is one dense block (sizes may differ between cells)
-  int n = a.nr;
-  std::vector<int> order(n);
-  for (int i = 0; i < n; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cells[x] < cells[y]; });
-  std::vector<int> idx, ioff{0};
-  std::vector<int64_t> moff{0};
-  int kmax = 0;
-  for (int s = 0; s < n;) {
-    int e = s;
-    while (e < n && cells[order[e]] == cells[order[s]]) ++e;
-    std::vector<int> g(order.begin() + s, order.begin() + e);
-    std::sort(g.begin(), g.end());
-    int k = (int)g.size();
-    if (k > 8) throw MgError(MG_ERR_UNSUPPORTED, "global_relax: per-cell blocks larger than 8");
-    kmax = std::max(kmax, k);
-    idx.insert(idx.end(), g.begin(), g.end());
-    ioff.push_back((int)idx.size());
-    moff.push_back(moff.back() + (int64_t)k * k);
-    s = e;
-  }
+// per-unknown owning cell: grouping on the device (mgr.py:219-224: unknowns grouped
+// by cell, ascending inside a group, groups in ascending cell order)
+__global__ void k_cells_unsorted(const int64_t *c, int n, int *flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > 0 && i < n && c[i] < c[i - 1]) *flag = 1;
+}
+__global__ void k_cell_heads(const int64_t *c, int n, int *head) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) head[i] = (i == 0 || c[i] != c[i - 1]) ? 1 : 0;
+}
+__global__ void k_cell_starts(const int *head, const int *seg, int n, int nblk, int *ioff) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && head[i]) ioff[seg[i]] = i;
+  if (i == 0) ioff[nblk] = n;
+}
+__global__ void k_block_sizes(const int *ioff, int nblk, int *ksq, int *kmax) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  const int k = ioff[b + 1] - ioff[b];
+  ksq[b] = k <= 8 ? k * k : 0;
+  atomicMax(kmax, k);
+}
+__global__ void k_gather_i64(int64_t *d, const int64_t *s, const int *idx, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = s[idx[i]];
+}
+
+static std::unique_ptr<BlockDiag> blockdiag_setup(const Csr &a, const int64_t *cells) {
+  // group unknowns by owning cell on the device: stable radix sort of (cell, index)
+  // unless the cells are already non-decreasing (cell-major numbering), run heads,
+  // block offsets; each group is one dense block (sizes may differ between cells)
+  const int n = a.nr;
   auto bd = std::make_unique<BlockDiag>();
-  bd->nblk = (int)ioff.size() - 1;
-  bd->kmax = kmax;
-  bd->idx.alloc(idx.size());
-  h2d(bd->idx.p, idx.data(), sizeof(int) * idx.size());
-  bd->ioff.alloc(ioff.size());
-  h2d(bd->ioff.p, ioff.data(), sizeof(int) * ioff.size());
-  bd->moff.alloc(moff.size());
-  h2d(bd->moff.p, moff.data(), sizeof(int64_t) * moff.size());
-  const int nblk = bd->nblk;
-  DBuf<double> blk((size_t)(moff.back() ? moff.back() : 1));
-  bd->inv.alloc((size_t)(moff.back() ? moff.back() : 1));
-  if (nblk) {
-    k_bd_gather<<<grid_for(nblk, 128), 128, 0, stream()>>>(nblk, bd->ioff.p, bd->moff.p, bd->idx.p, a.rp.p,
-                                                           a.ci.p, a.v.p, blk.p);
-    check_launch("bd_gather");
+  bd->idx.alloc((size_t)(n ? n : 1));
+  if (n == 0) {
+    bd->ioff.alloc(1);
+    dset_i32(bd->ioff.p, {0});
+    bd->moff.alloc(1);
+    dzero(bd->moff.p, sizeof(int64_t));
+    return bd;
   }
+  iota_i32(bd->idx.p, n);
+  DBuf<int> st(2);
+  dset_i32(st.p, {0, 0});
+  k_cells_unsorted<<<grid_for(n, 256), 256, 0, stream()>>>(cells, n, st.p);
+  check_launch("cells_unsorted");
+  int unsorted = 0;
+  d2h(&unsorted, st.p, sizeof(int));
+  DBuf<int64_t> sorted_cells;
+  const int64_t *keys = cells;
+  if (unsorted) {
+    sorted_cells.alloc(n);
+    DBuf<int> order(n);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, cells, sorted_cells.p, bd->idx.p, order.p, n, 0, 64, stream());
+    void *tmp = cub_scratch(tb);
+    MG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, cells, sorted_cells.p, bd->idx.p, order.p, n, 0, 64,
+                                            stream()));
+    count_launch(8);
+    std::swap(bd->idx, order);
+    keys = sorted_cells.p;
+  }
+  DBuf<int> head(n), seg((size_t)n + 1);
+  k_cell_heads<<<grid_for(n, 256), 256, 0, stream()>>>(keys, n, head.p);
+  check_launch("cell_heads");
+  const int nblk = (int)exclusive_scan_i32_to_i32(head.p, seg.p, n);
+  bd->nblk = nblk;
+  bd->ioff.alloc((size_t)nblk + 1);
+  k_cell_starts<<<grid_for(n, 256), 256, 0, stream()>>>(head.p, seg.p, n, nblk, bd->ioff.p);
+  check_launch("cell_starts");
+  DBuf<int> ksq(nblk);
+  k_block_sizes<<<grid_for(nblk, 256), 256, 0, stream()>>>(bd->ioff.p, nblk, ksq.p, st.p + 1);
+  check_launch("block_sizes");
+  bd->moff.alloc((size_t)nblk + 1);
+  const int64_t tot = exclusive_scan_i32_to_i64(ksq.p, bd->moff.p, nblk);
+  d2h(&bd->kmax, st.p + 1, sizeof(int));
+  if (bd->kmax > 8) throw MgError(MG_ERR_UNSUPPORTED, "global_relax: per-cell blocks larger than 8");
+  DBuf<double> blk((size_t)(tot ? tot : 1));
+  bd->inv.alloc((size_t)(tot ? tot : 1));
+  k_bd_gather<<<grid_for(nblk, 128), 128, 0, stream()>>>(nblk, bd->ioff.p, bd->moff.p, bd->idx.p, a.rp.p,
+                                                         a.ci.p, a.v.p, blk.p);
+  check_launch("bd_gather");
   DBuf<int> bad(1);
   const int big = 0x7fffffff;
   dset_i32(bad.p, {big});
-  if (nblk) {
-    k_bd_invert<<<grid_for(nblk, 64), 64, 0, stream()>>>(nblk, bd->ioff.p, bd->moff.p, blk.p, bd->inv.p, bad.p);
-    check_launch("bd_invert");
-  }
+  k_bd_invert<<<grid_for(nblk, 64), 64, 0, stream()>>>(nblk, bd->ioff.p, bd->moff.p, blk.p, bd->inv.p, bad.p);
+  check_launch("bd_invert");
   int hb;
   d2h(&hb, bad.p, sizeof(int));
   if (hb != big) throw MgError(MG_ERR_SINGULAR, "singular per-cell block", hb);
@@ -451,10 +544,16 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
     // per-unknown owning cell, tracked down the levels only when a level relaxes globally
     bool need_cells = false;
     for (const LevelSpec &sp : plan) need_cells |= sp.global_relax != 0;
-    std::vector<int64_t> cells;
+    DBuf<int64_t> cells;  // device copy, gathered down the levels by the C lists
     if (need_cells) {
-      cells.resize(a.nr);
-      for (int i = 0; i < a.nr; ++i) cells[i] = cells_host ? cells_host[i] : i;
+      cells.alloc((size_t)(a.nr ? a.nr : 1));
+      if (cells_host) {
+        h2d(cells.p, cells_host, sizeof(int64_t) * a.nr);
+      } else {
+        std::vector<int64_t> ident(a.nr);
+        for (int i = 0; i < a.nr; ++i) ident[i] = i;
+        h2d(cells.p, ident.data(), sizeof(int64_t) * a.nr);
+      }
     }
     for (const LevelSpec &sp : plan) {
       int n = cur.nr;
@@ -494,13 +593,14 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       trace("mgr: A*P");
       Csr ac = spgemm(lv.R, ap);
       trace("mgr: R*(AP)");
-      if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells);
+      if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells.p);
       if (need_cells) {
-        std::vector<int64_t> nxt_cells(lv.nc);
-        std::vector<int> cl(lv.nc);
-        d2h(cl.data(), lv.clist.p, sizeof(int) * lv.nc);
-        for (int c = 0; c < lv.nc; ++c) nxt_cells[c] = cells[cl[c]];
-        cells.swap(nxt_cells);
+        DBuf<int64_t> nxt((size_t)(lv.nc ? lv.nc : 1));
+        if (lv.nc) {
+          k_gather_i64<<<grid_for(lv.nc, 256), 256, 0, stream()>>>(nxt.p, cells.p, lv.clist.p, lv.nc);
+          check_launch("gather_cells");
+        }
+        std::swap(cells, nxt);
       }
       lv.A = std::move(cur);
       cur = std::move(ac);

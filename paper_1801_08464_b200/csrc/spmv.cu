@@ -793,6 +793,17 @@ static bool sell_pf() {
   return on;
 }
 
+// rows longer than this (average) take the UNR = 8 SELL kernel (software pipelined
+// with MG_SELL_PF) instead of UNR = 4; MG_SELL_LONG_AVG overrides (A/B)
+static double sell_long_avg() {
+  static double v = -1.0;
+  if (v < 0) {
+    const char *e = getenv("MG_SELL_LONG_AVG");
+    v = e ? atof(e) : 64.0;
+  }
+  return v;
+}
+
 template <class Epi, class XG = XPlain>
 static void launch_csr(const Csr &a, XG x, Epi epi) {
   if (a.nr == 0) return;
@@ -822,7 +833,7 @@ static void launch_csr(const Csr &a, XG x, Epi epi) {
       launch_pdl(k_sell<UNR, IK, false, Epi, XG>, grid_for(a.nr, T), T, 0, a.nr, pl.sptr.p, pl.rlen.p,         \
                  (const int *)pl.perm.p, ci, pl.dict.p, pl.mul, pl.sv.p, x, epi);                              \
   } while (0)
-    if (avg > 64) {
+    if (avg > sell_long_avg()) {
       if (pl.ik == 1) LAUNCH_SELL(8, 128, 1);
       else if (pl.ik == 2) LAUNCH_SELL(8, 128, 2);
       else LAUNCH_SELL(8, 128, 0);
