@@ -56,6 +56,21 @@ __global__ void k_gather(double *d, const double *s, const int *idx, int64_t n) 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     d[i] = s[idx[i]];
 }
+// dst = src[idx]; bs = sign .* dst (when sign); xo = d .* (bs or dst): the gather of
+// the F-residual fused with the first pre-sweep from zero of the F-relaxation AMG
+__global__ void k_gather_scale(double *dst, const double *src, const int *idx, int64_t n, const double *sign,
+                               double *bs, const double *dv, double *xo) {
+  PDL_ENTRY();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = src[idx[i]];
+    dst[i] = v;
+    if (sign) {
+      v = sign[i] * v;
+      bs[i] = v;
+    }
+    xo[i] = dv[i] * v;
+  }
+}
 __global__ void k_scatter_add(double *d, const double *s, const int *idx, int64_t n) {
   PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -118,6 +133,12 @@ void gather(double *dst, const double *src, const int *idx, int64_t n) {
   if (!n) return;
   launch_pdl(k_gather, ew_grid(n), 256, 0, dst, src, idx, n);
   check_launch("gather");
+}
+void gather_scale(double *dst, const double *src, const int *idx, int64_t n, const double *sign, double *bs,
+                  const double *d, double *xo) {
+  if (!n) return;
+  launch_pdl(k_gather_scale, ew_grid(n), 256, 0, dst, src, idx, n, sign, bs, d, xo);
+  check_launch("gather_scale");
 }
 void scatter_add(double *dst, const double *src, const int *idx, int64_t n) {
   if (!n) return;

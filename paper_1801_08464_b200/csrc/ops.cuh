@@ -15,6 +15,10 @@ void residual(const Csr &a, const double *x, const double *b, double *r);
 void spmv_add(const Csr &a, const double *x, double *y);
 // y = [ef scattered by fmap (fmap[i] < 0: 0)] + A x
 void spmv_merge_add(const Csr &a, const double *x, const int *fmap, const double *ef, double *y);
+// y = A x; bs = sign .* y (when sign); xo = d .* (bs or y): a restriction fused with
+// the coarser AMG level's first pre-sweep from zero (x = D^-1 b)
+void spmv_store_scale(const Csr &a, const double *x, double *y, const double *sign, double *bs, const double *d,
+                      double *xo);
 // xo = x + dinv .* (b - A x)   (L1-Jacobi sweep)
 void jacobi_sweep(const Csr &a, const double *x, const double *b, const double *dinv, double *xo);
 
@@ -28,6 +32,9 @@ void vdiv_scalar(double *y, const double *x, double d, int64_t n);          // y
 void vsub(double *r, const double *b, const double *ax, int64_t n);         // r = b - ax
 void gather(double *dst, const double *src, const int *idx, int64_t n);     // dst[i] = src[idx[i]]
 void scatter_add(double *dst, const double *src, const int *idx, int64_t n);// dst[idx[i]] += src[i]
+// dst = src[idx]; bs = sign .* dst (when sign); xo = d .* (bs or dst)
+void gather_scale(double *dst, const double *src, const int *idx, int64_t n, const double *sign, double *bs,
+                  const double *d, double *xo);
 void scatter_set(double *dst, const double *src, const int *idx, int64_t n);// dst[idx[i]] = src[i]
 // e[i] = fmap[i] >= 0 ? ef[fmap[i]] : 0   (F values into a zeroed full vector, one pass)
 void fc_merge(double *e, const double *ef, const int *fmap, int64_t n);

@@ -190,7 +190,20 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
   return h;
 }
 
-static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero) {
+// The buffer level l's first pre-sweep from zero writes (x = D^-1 b): every sweep
+// after it flips cur / oth, so it starts in the buffer that makes the last one land
+// in x (no copy-back launch).  Producers of b (the restriction from level l-1, the
+// MGR gather / restriction feeding the hierarchy) write x = D^-1 b there directly.
+static double *first_buf(Amg &h, int l, double *x) {
+  const int flips = (h.opts.pre > 0 ? h.opts.pre - 1 : 0) + h.opts.post;
+  return (flips & 1) ? h.L[l].t.p : x;
+}
+static bool fused_pre(const Amg &h, int l) {  // level l has a pre-sweep that a producer can form
+  return h.opts.pre > 0 && l + 1 < (int)h.L.size();
+}
+
+// pre_done: x_zero and the first pre-sweep's result is already in first_buf(l, x)
+static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero, bool pre_done = false) {
   ProfScope plev(level_prof() && l < 50 ? 100 + (h.tag_k0 ? 0 : 50) + l : -1);
   AmgLevel &v = h.L[l];
   if (l + 1 == (int)h.L.size()) {
@@ -199,16 +212,11 @@ static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero) {
   }
   AmgLevel &nx = h.L[l + 1];
   double *cur = x, *oth = v.t.p;
-  if (x_zero) {
-    // every sweep after the zero start flips cur / oth: start in the buffer that
-    // makes the last one land in x, so no copy-back launch is needed
-    const int flips = (h.opts.pre > 0 ? h.opts.pre - 1 : 0) + h.opts.post;
-    if (flips & 1) std::swap(cur, oth);
-  }
+  if (x_zero && first_buf(h, l, x) != x) std::swap(cur, oth);
   const int k0 = (h.tag_k0 && l == 0) ? 8 : -1;  // timed as the dominant kernel when profiling
   for (int s = 0; s < h.opts.pre; ++s) {
     if (x_zero) {
-      vmul(cur, v.l1inv.p, b, v.n);
+      if (!pre_done) vmul(cur, v.l1inv.p, b, v.n);
       x_zero = false;
     } else {
       ProfScope ps(k0);
@@ -221,8 +229,10 @@ static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero) {
     residual(v.A, cur, b, v.r.p);
     res = v.r.p;
   }
-  spmv(v.R, res, nx.b.p);
-  vcycle(h, l + 1, nx.b.p, nx.x.p, true);
+  const bool fuse = fused_pre(h, l + 1);
+  if (fuse) spmv_store_scale(v.R, res, nx.b.p, nullptr, nullptr, nx.l1inv.p, first_buf(h, l + 1, nx.x.p));
+  else spmv(v.R, res, nx.b.p);
+  vcycle(h, l + 1, nx.b.p, nx.x.p, true, fuse);
   if (x_zero) spmv(v.P, nx.x.p, cur);
   else spmv_add(v.P, nx.x.p, cur);
   for (int s = 0; s < h.opts.post; ++s) {
@@ -233,24 +243,35 @@ static void vcycle(Amg &h, int l, const double *b, double *x, bool x_zero) {
   if (cur != x) vcopy(x, cur, v.n);
 }
 
-void amg_vcycle(Amg &h, const double *b, const double *x0, double *x) {
+AmgPreTargets amg_pre_targets(Amg &h, double *x) {
+  AmgPreTargets t;
+  if (!fused_pre(h, 0)) return t;
+  t.ok = true;
+  t.sign = h.has_sign ? h.sign.p : nullptr;
+  t.bs = h.has_sign ? h.L[0].b.p : nullptr;
+  t.d = h.L[0].l1inv.p;
+  t.xo = first_buf(h, 0, x);
+  return t;
+}
+
+void amg_vcycle(Amg &h, const double *b, const double *x0, double *x, bool pre_done) {
   AmgLevel &l0 = h.L[0];
   const double *bb = b;
   if (h.has_sign) {
-    vmul(l0.b.p, h.sign.p, b, l0.n);
+    if (!pre_done) vmul(l0.b.p, h.sign.p, b, l0.n);
     bb = l0.b.p;
   }
   if (x0) {
     if (x0 != x) vcopy(x, x0, l0.n);
     vcycle(h, 0, bb, x, false);
   } else {
-    vcycle(h, 0, bb, x, true);
+    vcycle(h, 0, bb, x, true, pre_done);
   }
 }
 
-void amg_apply(Amg &h, const double *b, double *x) {
+void amg_apply(Amg &h, const double *b, double *x, bool pre_done) {
   ProfScope ps(1);
-  amg_vcycle(h, b, nullptr, x);
+  amg_vcycle(h, b, nullptr, x, pre_done);
   for (int c = 1; c < h.opts.cycles; ++c) amg_vcycle(h, b, x, x);
 }
 
@@ -293,7 +314,7 @@ static void fsolver_setup(FSolver &fs, Csr &aff, const LevelSpec &sp, const AmgO
   }
 }
 
-static void fsolve(FSolver &fs, const Csr &aff, const double *r, double *x) {
+static void fsolve(FSolver &fs, const Csr &aff, const double *r, double *x, bool pre_done = false) {
   if (fs.kind == FR_JACOBI) {
     vmul(x, fs.invd.p, r, fs.nf);
     double *cur = x, *oth = fs.t1.p;
@@ -303,7 +324,7 @@ static void fsolve(FSolver &fs, const Csr &aff, const double *r, double *x) {
     }
     if (cur != x) vcopy(x, cur, fs.nf);
   } else if (fs.kind == FR_AMG) {
-    amg_vcycle(*fs.amg, r, nullptr, x);
+    amg_vcycle(*fs.amg, r, nullptr, x, pre_done);
   } else if (fs.kind == FR_GS) {
     // x = L^-1 r; x += L^-1 (r - A_ff x) per further sweep (mgr.py:185-188)
     trsv_lower(fs.tril, r, x, fs.ctrl.p);
@@ -661,9 +682,9 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
   return h;
 }
 
-static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
+static void apply_level(Mgr &h, size_t k, const double *r, double *e, bool pre_done = false) {
   if (k == h.L.size()) {
-    if (h.coarse_kind == 0) amg_apply(*h.camg, r, e);
+    if (h.coarse_kind == 0) amg_apply(*h.camg, r, e, pre_done);
     else dense_matvec(h.cinv.p, r, e, h.cn);
     return;
   }
@@ -684,14 +705,20 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
     return lv.res.p;
   };
   auto f_relax = [&]() {
+    bool pre = false;
     {
       ProfScope ps(4);
       const double *rr = resid();
-      gather(lv.rF.p, rr, lv.flist.p, lv.nf);
+      // the F-relaxation AMG's first pre-sweep (x = D^-1 r_F) is formed by the gather
+      AmgPreTargets t;
+      if (lv.fs.kind == FR_AMG) t = amg_pre_targets(*lv.fs.amg, lv.eF.p);
+      if (t.ok) gather_scale(lv.rF.p, rr, lv.flist.p, lv.nf, t.sign, t.bs, t.d, t.xo);
+      else gather(lv.rF.p, rr, lv.flist.p, lv.nf);
+      pre = t.ok;
     }
     {
       ProfScope ps(2);
-      fsolve(lv.fs, lv.Aff, lv.rF.p, lv.eF.p);
+      fsolve(lv.fs, lv.Aff, lv.rF.p, lv.eF.p, pre);
       if (g_ctx->profiling && lv.fs.amg) {
         g_ctx->timing.frelax_calls++;
         g_ctx->timing.frelax_bytes += lv.fs.amg->cycle_bytes();
@@ -711,12 +738,18 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e) {
     zero = false;
   };
   auto coarse_correct = [&]() {
+    bool pre = false;
     {
       ProfScope ps(4);
       const double *rr = resid();
-      spmv(lv.R, rr, lv.rc.p);
+      // restriction into the coarse AMG: its first pre-sweep is formed in the epilogue
+      AmgPreTargets t;
+      if (k + 1 == h.L.size() && h.coarse_kind == 0) t = amg_pre_targets(*h.camg, lv.ec.p);
+      if (t.ok) spmv_store_scale(lv.R, rr, lv.rc.p, t.sign, t.bs, t.d, t.xo);
+      else spmv(lv.R, rr, lv.rc.p);
+      pre = t.ok;
     }
-    apply_level(h, k + 1, lv.rc.p, lv.ec.p);
+    apply_level(h, k + 1, lv.rc.p, lv.ec.p, pre);
     ProfScope ps(4);
     if (zero) spmv(lv.P, lv.ec.p, e);
     else if (!merged) spmv_merge_add(lv.P, lv.ec.p, lv.fmap.p, lv.eF.p, e);

@@ -36,8 +36,18 @@ struct Amg {
 };
 
 std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o);
-void amg_vcycle(Amg &h, const double *b, const double *x0, double *x);
-void amg_apply(Amg &h, const double *b, double *x);
+// pre_done (x0 == nullptr only): the producer of b already formed the first
+// pre-sweep from zero at the targets amg_pre_targets(h, x) returned
+void amg_vcycle(Amg &h, const double *b, const double *x0, double *x, bool pre_done = false);
+void amg_apply(Amg &h, const double *b, double *x, bool pre_done = false);
+struct AmgPreTargets {
+  bool ok = false;             // the hierarchy has a level-0 pre-sweep a producer can form
+  const double *sign = nullptr;
+  double *bs = nullptr;        // sign-normalised b (level-0 b buffer) when sign
+  const double *d = nullptr;   // level-0 L1 inverse
+  double *xo = nullptr;        // where the first pre-sweep writes for output x
+};
+AmgPreTargets amg_pre_targets(Amg &h, double *x);
 
 enum { RP_INJECTIVE = 0, RP_NONINJECTIVE = 1, RP_INJECTION = 2, RP_IDEAL = 3 };
 enum { FR_JACOBI = 0, FR_GS = 1, FR_AMG = 2, FR_EXACT = 3 };

@@ -216,6 +216,7 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
   if (u <= 32) nzc = emit_sorted<1>(t, mask, u, lane, oci + o, ov + o);
   else if (u <= 64) nzc = emit_sorted<2>(t, mask, u, lane, oci + o, ov + o);
   else if (u <= 128) nzc = emit_sorted<4>(t, mask, u, lane, oci + o, ov + o);
+  else if (T >= 512 && u <= 256) nzc = emit_sorted<8>(t, mask, u, lane, oci + o, ov + o);
   else {
     int P = 32;
     while (P < u) P <<= 1;

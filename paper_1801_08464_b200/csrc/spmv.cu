@@ -36,6 +36,23 @@ struct EpiMergeAdd {
     y[r] = (f >= 0 ? ef[f] : 0.0) + s;
   }
 };
+// y = A x with the next level's first pre-sweep from zero folded in (same products
+// as vmul: bs = sign * y, xo = d * bs)
+struct EpiStoreScale {
+  double *y;
+  const double *sign;
+  double *bs;
+  const double *d;
+  double *xo;
+  __device__ void operator()(int r, double s) const {
+    y[r] = s;
+    if (sign) {
+      s = sign[r] * s;
+      bs[r] = s;
+    }
+    xo[r] = d[r] * s;
+  }
+};
 struct EpiJacobi {
   const double *x, *b, *dinv;
   double *xo;
@@ -914,6 +931,12 @@ void spmv_merge_add(const Csr &a, const double *x, const int *fmap, const double
 void spmv_add(const Csr &a, const double *x, double *y) {
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spmv_add: scalar CSR only");
   launch_csr(a, XPlain{x}, EpiAdd{y});
+}
+
+void spmv_store_scale(const Csr &a, const double *x, double *y, const double *sign, double *bs, const double *d,
+                      double *xo) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spmv_store_scale: scalar CSR only");
+  launch_csr(a, XPlain{x}, EpiStoreScale{y, sign, bs, d, xo});
 }
 
 void jacobi_sweep(const Csr &a, const double *x, const double *b, const double *dinv, double *xo) {
