@@ -147,7 +147,7 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
     trace("  ext_interp");
     Csr r = transpose(p);
     trace("  transpose");
-    Csr ap = spgemm(cur.A, p);
+    Csr ap = spgemm(cur.A, p, false);  // intermediate: R*(AP) sums do not depend on its order
     trace("  A*P");
     Csr ac = spgemm(r, ap);
     trace("  R*(AP)");
@@ -610,7 +610,7 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       }
       build_rp(cur, fmap.p, cmap.p, lv.flist.p, lv.clist.p, lv.nf, lv.nc, sp.rp, lv.R, lv.P);
       trace("mgr: build_rp");
-      Csr ap = spgemm(cur, lv.P);
+      Csr ap = spgemm(cur, lv.P, false);
       trace("mgr: A*P");
       Csr ac = spgemm(lv.R, ap);
       trace("mgr: R*(AP)");

@@ -4,7 +4,10 @@
 
 namespace mg {
 // C = A B, scipy csr_matmat semantics (exact zeros dropped, sorted columns)
-Csr spgemm(const Csr &a, const Csr &b);
+// C = A B with scipy csr_matmat sums; sorted = false leaves each row's columns in
+// hash-slot order (only for an intermediate consumed as the right factor of another
+// product, whose sums do not depend on that order)
+Csr spgemm(const Csr &a, const Csr &b, bool sorted = true);
 // A^T with ascending columns per row
 Csr transpose(const Csr &a);
 // rows_dev: nr source rows (sorted); cmap_dev: column map (source col -> new col or -1)

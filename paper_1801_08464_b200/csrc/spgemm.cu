@@ -174,6 +174,7 @@ __device__ __forceinline__ int emit_sorted(const FillTabs &t, unsigned mask, int
   return nzc;
 }
 
+template <bool SORT>
 __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, const int *arp, const int *aci,
                                          const double *av, const int *brp, const int *bci, const double *bv,
                                          const int64_t *base, int *oci, double *ov, int *nz) {
@@ -201,35 +202,56 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
     }
     __syncwarp();
   });
-  // sorted key list
-  int filled = 0;
-  for (int i0 = 0; i0 < T; i0 += 32) {
-    int k = t.keys[i0 + lane];
-    unsigned bal = __ballot_sync(0xffffffffu, k != -1);
-    if (k != -1) t.list[filled + __popc(bal & ((1u << lane) - 1))] = k;
-    filled += __popc(bal);
-  }
-  __syncwarp();
   int64_t o = base[row];
-  MG_DCHECK(filled == u && u <= T / 2);  // list capacity; u = the count pass's size
   int nzc = 0;
-  if (u <= 32) nzc = emit_sorted<1>(t, mask, u, lane, oci + o, ov + o);
-  else if (u <= 64) nzc = emit_sorted<2>(t, mask, u, lane, oci + o, ov + o);
-  else if (u <= 128) nzc = emit_sorted<4>(t, mask, u, lane, oci + o, ov + o);
-  else if (T >= 512 && u <= 256) nzc = emit_sorted<8>(t, mask, u, lane, oci + o, ov + o);
-  else {
-    int P = 32;
-    while (P < u) P <<= 1;
-    MG_DCHECK(P <= T / 2);
-    for (int i = u + lane; i < P; i += 32) t.list[i] = 0x7fffffff;
+  if (!SORT) {
+    // unsorted output (a Galerkin intermediate A*P: R*(AP) accumulates each of its
+    // output columns in R's row order whatever the column order inside AP's rows,
+    // so only the final product needs scipy's sorted layout): slot order, values
+    // straight from the table, no key list / sort / probe
+    int filled = 0;
+    for (int i0 = 0; i0 < T; i0 += 32) {
+      const int k = t.keys[i0 + lane];
+      const unsigned bal = __ballot_sync(0xffffffffu, k != -1);
+      if (k != -1) {
+        const int q = filled + __popc(bal & ((1u << lane) - 1));
+        const double val = t.acc[i0 + lane];
+        oci[o + q] = k;
+        ov[o + q] = val;
+        nzc += val != 0.0;
+      }
+      filled += __popc(bal);
+    }
+    MG_DCHECK(filled == u);
+  } else {
+    // sorted key list
+    int filled = 0;
+    for (int i0 = 0; i0 < T; i0 += 32) {
+      int k = t.keys[i0 + lane];
+      unsigned bal = __ballot_sync(0xffffffffu, k != -1);
+      if (k != -1) t.list[filled + __popc(bal & ((1u << lane) - 1))] = k;
+      filled += __popc(bal);
+    }
     __syncwarp();
-    warp_bitonic(t.list, P, lane);
-    for (int q = lane; q < u; q += 32) {
-      int k = t.list[q];
-      double val = t.acc[hash_find(t.keys, mask, k)];
-      oci[o + q] = k;
-      ov[o + q] = val;
-      nzc += val != 0.0;
+    MG_DCHECK(filled == u && u <= T / 2);  // list capacity; u = the count pass's size
+    if (u <= 32) nzc = emit_sorted<1>(t, mask, u, lane, oci + o, ov + o);
+    else if (u <= 64) nzc = emit_sorted<2>(t, mask, u, lane, oci + o, ov + o);
+    else if (u <= 128) nzc = emit_sorted<4>(t, mask, u, lane, oci + o, ov + o);
+    else if (T >= 512 && u <= 256) nzc = emit_sorted<8>(t, mask, u, lane, oci + o, ov + o);
+    else {
+      int P = 32;
+      while (P < u) P <<= 1;
+      MG_DCHECK(P <= T / 2);
+      for (int i = u + lane; i < P; i += 32) t.list[i] = 0x7fffffff;
+      __syncwarp();
+      warp_bitonic(t.list, P, lane);
+      for (int q = lane; q < u; q += 32) {
+        int k = t.list[q];
+        double val = t.acc[hash_find(t.keys, mask, k)];
+        oci[o + q] = k;
+        ov[o + q] = val;
+        nzc += val != 0.0;
+      }
     }
   }
   for (int off = 16; off > 0; off >>= 1) nzc += __shfl_xor_sync(0xffffffffu, nzc, off);
@@ -240,7 +262,7 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
 template <int T>
 __host__ __device__ constexpr size_t fill_bytes() { return (size_t)T * 4 + (size_t)T * 8 + (size_t)T * 2 + 256; }
 
-template <int T, int WPB>
+template <int T, int WPB, bool SORT>
 __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_fill(int nrows, const int *rows, const int *arp,
                                                           const int *aci, const double *av, const int *brp,
                                                           const int *bci, const double *bv, const int64_t *base,
@@ -254,9 +276,10 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_fill(int
   t.keys = (int *)(t.win + 32);
   t.list = t.keys + T;
   for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB)
-    fill_row(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
+    fill_row<SORT>(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
 }
 
+template <bool SORT>
 __global__ void k_spgemm_fill_g(int nrows, const int *rows, const int64_t *goff, const int *gsize,
                                 unsigned char *pool, const int *arp, const int *aci, const double *av,
                                 const int *brp, const int *bci, const double *bv, const int64_t *base, int *oci,
@@ -270,7 +293,7 @@ __global__ void k_spgemm_fill_g(int nrows, const int *rows, const int64_t *goff,
   t.win = t.acc + T;
   t.keys = (int *)(t.win + 32);
   t.list = t.keys + T;
-  fill_row(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
+  fill_row<SORT>(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
 }
 
 // compaction: drop exact zeros, keep order (VS-lane group per row)
@@ -407,15 +430,21 @@ static void launch_count(int nrows, const int *rows, const Csr &a, const Csr &b,
   check_launch("spgemm_count");
 }
 
+template <int T, int WPB, bool SORT>
+static void launch_fill_t(int nrows, const int *rows, const Csr &a, const Csr &b, const int64_t *base, int *oci,
+                          double *ov, int *nz) {
+  size_t sm = fill_bytes<T>() * WPB;
+  MG_CUDA(cudaFuncSetAttribute(k_spgemm_fill<T, WPB, SORT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_spgemm_fill<T, WPB, SORT><<<cap_grid(nrows, WPB), WPB * 32, sm, stream()>>>(
+      nrows, rows, a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, base, oci, ov, nz);
+  check_launch("spgemm_fill");
+}
 template <int T, int WPB>
 static void launch_fill(int nrows, const int *rows, const Csr &a, const Csr &b, const int64_t *base, int *oci,
-                        double *ov, int *nz) {
+                        double *ov, int *nz, bool sorted) {
   if (!nrows) return;
-  size_t sm = fill_bytes<T>() * WPB;
-  MG_CUDA(cudaFuncSetAttribute(k_spgemm_fill<T, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_spgemm_fill<T, WPB><<<cap_grid(nrows, WPB), WPB * 32, sm, stream()>>>(nrows, rows, a.rp.p, a.ci.p, a.v.p,
-                                                                          b.rp.p, b.ci.p, b.v.p, base, oci, ov, nz);
-  check_launch("spgemm_fill");
+  if (sorted) launch_fill_t<T, WPB, true>(nrows, rows, a, b, base, oci, ov, nz);
+  else launch_fill_t<T, WPB, false>(nrows, rows, a, b, base, oci, ov, nz);
 }
 
 static bool fill_sparse_tables() {  // MG_SPGEMM_SPARSE=0: load factor 1/2 in every bin (A/B)
@@ -427,7 +456,7 @@ static bool fill_sparse_tables() {  // MG_SPGEMM_SPARSE=0: load factor 1/2 in ev
   return on;
 }
 
-Csr spgemm(const Csr &a, const Csr &b) {
+Csr spgemm(const Csr &a, const Csr &b, bool sorted) {
   if (a.b != 1 || b.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spgemm: scalar CSR only");
   if (a.nc != b.nr) throw MgError(MG_ERR_DIM_MISMATCH, "matmul: inner dimensions differ");
   int m = a.nr;
@@ -469,7 +498,8 @@ Csr spgemm(const Csr &a, const Csr &b) {
     // fill pass, tables sized by the exact distinct count
     RowBins bins;
     bins.build(cnt.p, m, 2);
-#define FB(k, T, W) launch_fill<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, trp.p, tci.p, tv.p, nz.p)
+#define FB(k, T, W) \
+  launch_fill<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, trp.p, tci.p, tv.p, nz.p, sorted)
     if (fill_sparse_tables()) {
       // load factor <= 1/4 for the two small bins (shorter probe runs: fill 9.7 ->
       // 8.8 ms and 11.1 -> 9.5 ms at 128^3); larger tables cost more in occupancy
@@ -489,7 +519,8 @@ Csr spgemm(const Csr &a, const Csr &b) {
 #undef FB
     int ng = bins.cnt[NBIN];
     if (ng) {
-      k_spgemm_fill_g<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
+      auto kern = sorted ? k_spgemm_fill_g<true> : k_spgemm_fill_g<false>;
+      kern<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
           ng, bins.rows.p + bins.off[NBIN], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, a.v.p, b.rp.p,
           b.ci.p, b.v.p, trp.p, tci.p, tv.p, nz.p);
       check_launch("spgemm_fill_g");

@@ -821,6 +821,15 @@ static double sell_long_avg() {
   return v;
 }
 
+static int csr_long_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MG_CSR_LONG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <class Epi, class XG = XPlain>
 static void launch_csr(const Csr &a, XG x, Epi epi) {
   if (a.nr == 0) return;
@@ -874,7 +883,15 @@ static void launch_csr(const Csr &a, XG x, Epi epi) {
   // for the ~100-150/row coarse-AMG levels (76 -> 84%)
   else if (avg <= 36) LAUNCH_AVG(8, 2);
   else if (avg <= 72) LAUNCH_AVG(8, 4);
-  else LAUNCH_AVG(16, 4);
+  else {
+    switch (csr_long_variant()) {  // MG_CSR_LONG (A/B of the lane split for > 72 per row)
+      case 1: LAUNCH_AVG(16, 8); break;
+      case 2: LAUNCH_AVG(32, 4); break;
+      case 3: LAUNCH_AVG(32, 2); break;
+      case 4: LAUNCH_AVG(8, 8); break;
+      default: LAUNCH_AVG(16, 4);
+    }
+  }
 #undef LAUNCH_AVG
   check_launch("csr spmv");
 }
