@@ -287,7 +287,7 @@ int mg_triple_product(mg_ctx *ctx, const mg_mat *r, const mg_mat *a, const mg_ma
       throw MgError(MG_ERR_DIM_MISMATCH, "triple_product: inner dimensions differ");
     Csr ap = spgemm(C(a), C(p), false);
     auto *m = new mg_mat();
-    try { m->m = spgemm(C(r), ap); } catch (...) { delete m; throw; }
+    try { m->m = spgemm(C(r), ap, true, true); } catch (...) { delete m; throw; }
     *out = m;
   });
 }

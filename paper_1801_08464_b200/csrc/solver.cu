@@ -149,7 +149,7 @@ std::unique_ptr<Amg> amg_setup(const Csr &a, const AmgOpts &o) {
     trace("  transpose");
     Csr ap = spgemm(cur.A, p, false);  // intermediate: R*(AP) sums do not depend on its order
     trace("  A*P");
-    Csr ac = spgemm(r, ap);
+    Csr ac = spgemm(r, ap, true, true);
     trace("  R*(AP)");
     cur.P = std::move(p);
     cur.R = std::move(r);
@@ -612,7 +612,7 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       trace("mgr: build_rp");
       Csr ap = spgemm(cur, lv.P, false);
       trace("mgr: A*P");
-      Csr ac = spgemm(lv.R, ap);
+      Csr ac = spgemm(lv.R, ap, true, true);
       trace("mgr: R*(AP)");
       if (sp.global_relax) lv.bd = blockdiag_setup(cur, cells.p);
       if (need_cells) {

@@ -7,7 +7,9 @@ namespace mg {
 // C = A B with scipy csr_matmat sums; sorted = false leaves each row's columns in
 // hash-slot order (only for an intermediate consumed as the right factor of another
 // product, whose sums do not depend on that order)
-Csr spgemm(const Csr &a, const Csr &b, bool sorted = true);
+// b_unique: B's rows hold distinct columns (a product formed here), enabling the
+// conflict-free one-B-row windows for long B rows
+Csr spgemm(const Csr &a, const Csr &b, bool sorted = true, bool b_unique = false);
 // A^T with ascending columns per row
 Csr transpose(const Csr &a);
 // rows_dev: nr source rows (sorted); cmap_dev: column map (source col -> new col or -1)

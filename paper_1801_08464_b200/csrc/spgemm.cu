@@ -97,8 +97,48 @@ __device__ __forceinline__ void for_products(int row, int lane, const int *__res
   }
 }
 
+// The same products, in the same order, but windows never span two A entries: the
+// products of one window come from one row of B, whose columns are distinct, so no
+// two lanes of a window share an output column (no conflict groups to serialise).
+// For long B rows (the Galerkin R*(AP)); lanes idle in a row's last window.
+template <bool NEED_VAL, class F>
+__device__ __forceinline__ void for_products_rows(int row, int lane, const int *__restrict__ arp,
+                                                  const int *__restrict__ aci, const double *__restrict__ av,
+                                                  const int *__restrict__ brp, const int *__restrict__ bci,
+                                                  const double *__restrict__ bv, F &&f) {
+  int s = arp[row], e = arp[row + 1];
+  for (int q0 = s; q0 < e; q0 += 32) {
+    int q = q0 + lane;
+    int rb = 0, len = 0;
+    double a = 0.0;
+    if (q < e) {
+      int j = __ldg(aci + q);
+      if (NEED_VAL) a = __ldg(av + q);
+      rb = __ldg(brp + j);
+      len = __ldg(brp + j + 1) - rb;
+    }
+    const int nq = min(32, e - q0);
+    for (int src = 0; src < nq; ++src) {
+      const int s_rb = __shfl_sync(0xffffffffu, rb, src);
+      const int s_len = __shfl_sync(0xffffffffu, len, src);
+      const double s_a = NEED_VAL ? __shfl_sync(0xffffffffu, a, src) : 0.0;
+      for (int w0 = 0; w0 < s_len; w0 += 32) {
+        const int p = w0 + lane;
+        const bool valid = p < s_len;
+        int k = -1;
+        double prod = 0.0;
+        if (valid) {
+          k = __ldg(bci + s_rb + p);
+          if (NEED_VAL) prod = __dmul_rn(s_a, __ldg(bv + s_rb + p));
+        }
+        f(valid, k, prod);
+      }
+    }
+  }
+}
+
 // ---- count pass: keys only ------------------------------------------------------
-template <int T, int WPB>
+template <int T, int WPB, bool RW>
 __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_count(int nrows, const int *rows, const int *arp,
                                                            const int *aci, const int *brp, const int *bci,
                                                            int *cnt) {
@@ -111,9 +151,11 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_count(in
     for (int i = lane; i < T; i += 32) keys[i] = -1;
     __syncwarp();
     int mine = 0;
-    for_products<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, [&](bool valid, int k, double) {
+    auto ins = [&](bool valid, int k, double) {
       if (valid) mine += hash_insert(keys, mask, k);
-    });
+    };
+    if (RW) for_products_rows<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, ins);
+    else for_products<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, ins);
     for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
     if (lane == 0) cnt[row] = mine;
     __syncwarp();
@@ -121,6 +163,7 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_count(in
 }
 
 // global-memory keys for rows beyond the largest smem bin
+template <bool RW>
 __global__ void k_spgemm_count_g(int nrows, const int *rows, const int64_t *goff, const int *gsize,
                                  unsigned char *pool, const int *arp, const int *aci, const int *brp,
                                  const int *bci, int *cnt) {
@@ -133,9 +176,11 @@ __global__ void k_spgemm_count_g(int nrows, const int *rows, const int64_t *goff
   for (int i = lane; i < T; i += 32) keys[i] = -1;
   __syncwarp();
   int mine = 0;
-  for_products<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, [&](bool valid, int k, double) {
+  auto ins = [&](bool valid, int k, double) {
     if (valid) mine += hash_insert(keys, mask, k);
-  });
+  };
+  if (RW) for_products_rows<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, ins);
+  else for_products<false>(row, lane, arp, aci, nullptr, brp, bci, nullptr, ins);
   for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
   if (lane == 0) cnt[row] = mine;
 }
@@ -174,7 +219,7 @@ __device__ __forceinline__ int emit_sorted(const FillTabs &t, unsigned mask, int
   return nzc;
 }
 
-template <bool SORT>
+template <bool SORT, bool RW>
 __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, const int *arp, const int *aci,
                                          const double *av, const int *brp, const int *bci, const double *bv,
                                          const int64_t *base, int *oci, double *ov, int *nz) {
@@ -182,26 +227,39 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
   for (int i = lane; i < T; i += 32) t.keys[i] = -1;
   __syncwarp();
   int u = 0;
-  for_products<true>(row, lane, arp, aci, av, brp, bci, bv, [&](bool valid, int k, double prod) {
-    int fresh = 0;
-    int slot = valid ? hash_insert_slot(t.keys, mask, k, &fresh) : -1 - lane;
-    if (fresh) t.acc[slot] = 0.0;
-    t.win[lane] = prod;
-    u += __popc(__ballot_sync(0xffffffffu, fresh));
-    unsigned grp = __match_any_sync(0xffffffffu, slot);
-    __syncwarp();
-    if (valid && lane == __ffs(grp) - 1) {
-      double sacc = t.acc[slot];
-      unsigned m = grp;
-      while (m) {
-        int l = __ffs(m) - 1;
-        sacc = __dadd_rn(sacc, t.win[l]);
-        m &= m - 1;
+  if (RW) {
+    // conflict-free windows (one B row each): every lane owns its slot in the window
+    for_products_rows<true>(row, lane, arp, aci, av, brp, bci, bv, [&](bool valid, int k, double prod) {
+      int fresh = 0;
+      if (valid) {
+        const int slot = hash_insert_slot(t.keys, mask, k, &fresh);
+        t.acc[slot] = __dadd_rn(fresh ? 0.0 : t.acc[slot], prod);
       }
-      t.acc[slot] = sacc;
-    }
-    __syncwarp();
-  });
+      u += __popc(__ballot_sync(0xffffffffu, fresh));
+      __syncwarp();
+    });
+  } else {
+    for_products<true>(row, lane, arp, aci, av, brp, bci, bv, [&](bool valid, int k, double prod) {
+      int fresh = 0;
+      int slot = valid ? hash_insert_slot(t.keys, mask, k, &fresh) : -1 - lane;
+      if (fresh) t.acc[slot] = 0.0;
+      t.win[lane] = prod;
+      u += __popc(__ballot_sync(0xffffffffu, fresh));
+      unsigned grp = __match_any_sync(0xffffffffu, slot);
+      __syncwarp();
+      if (valid && lane == __ffs(grp) - 1) {
+        double sacc = t.acc[slot];
+        unsigned m = grp;
+        while (m) {
+          int l = __ffs(m) - 1;
+          sacc = __dadd_rn(sacc, t.win[l]);
+          m &= m - 1;
+        }
+        t.acc[slot] = sacc;
+      }
+      __syncwarp();
+    });
+  }
   int64_t o = base[row];
   int nzc = 0;
   if (!SORT) {
@@ -262,7 +320,7 @@ __device__ __forceinline__ void fill_row(int row, int T, FillTabs t, int lane, c
 template <int T>
 __host__ __device__ constexpr size_t fill_bytes() { return (size_t)T * 4 + (size_t)T * 8 + (size_t)T * 2 + 256; }
 
-template <int T, int WPB, bool SORT>
+template <int T, int WPB, bool SORT, bool RW>
 __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_fill(int nrows, const int *rows, const int *arp,
                                                           const int *aci, const double *av, const int *brp,
                                                           const int *bci, const double *bv, const int64_t *base,
@@ -276,10 +334,10 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spgemm_fill(int
   t.keys = (int *)(t.win + 32);
   t.list = t.keys + T;
   for (int r = blockIdx.x * WPB + wid; r < nrows; r += gridDim.x * WPB)
-    fill_row<SORT>(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
+    fill_row<SORT, RW>(rows[r], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
 }
 
-template <bool SORT>
+template <bool SORT, bool RW>
 __global__ void k_spgemm_fill_g(int nrows, const int *rows, const int64_t *goff, const int *gsize,
                                 unsigned char *pool, const int *arp, const int *aci, const double *av,
                                 const int *brp, const int *bci, const double *bv, const int64_t *base, int *oci,
@@ -293,7 +351,7 @@ __global__ void k_spgemm_fill_g(int nrows, const int *rows, const int64_t *goff,
   t.win = t.acc + T;
   t.keys = (int *)(t.win + 32);
   t.list = t.keys + T;
-  fill_row<SORT>(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
+  fill_row<SORT, RW>(rows[wid], T, t, lane, arp, aci, av, brp, bci, bv, base, oci, ov, nz);
 }
 
 // compaction: drop exact zeros, keep order (VS-lane group per row)
@@ -423,28 +481,31 @@ static int cap_grid(int nrows, int wpb) {
 }
 
 template <int T, int WPB>
-static void launch_count(int nrows, const int *rows, const Csr &a, const Csr &b, int *cnt) {
+static void launch_count(int nrows, const int *rows, const Csr &a, const Csr &b, int *cnt, bool rw) {
   if (!nrows) return;
-  k_spgemm_count<T, WPB><<<cap_grid(nrows, WPB), WPB * 32, 0, stream()>>>(nrows, rows, a.rp.p, a.ci.p, b.rp.p,
-                                                                          b.ci.p, cnt);
+  auto kern = rw ? k_spgemm_count<T, WPB, true> : k_spgemm_count<T, WPB, false>;
+  kern<<<cap_grid(nrows, WPB), WPB * 32, 0, stream()>>>(nrows, rows, a.rp.p, a.ci.p, b.rp.p, b.ci.p, cnt);
   check_launch("spgemm_count");
 }
 
-template <int T, int WPB, bool SORT>
+template <int T, int WPB, bool SORT, bool RW>
 static void launch_fill_t(int nrows, const int *rows, const Csr &a, const Csr &b, const int64_t *base, int *oci,
                           double *ov, int *nz) {
   size_t sm = fill_bytes<T>() * WPB;
-  MG_CUDA(cudaFuncSetAttribute(k_spgemm_fill<T, WPB, SORT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  k_spgemm_fill<T, WPB, SORT><<<cap_grid(nrows, WPB), WPB * 32, sm, stream()>>>(
+  MG_CUDA(cudaFuncSetAttribute(k_spgemm_fill<T, WPB, SORT, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm));
+  k_spgemm_fill<T, WPB, SORT, RW><<<cap_grid(nrows, WPB), WPB * 32, sm, stream()>>>(
       nrows, rows, a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, base, oci, ov, nz);
   check_launch("spgemm_fill");
 }
 template <int T, int WPB>
 static void launch_fill(int nrows, const int *rows, const Csr &a, const Csr &b, const int64_t *base, int *oci,
-                        double *ov, int *nz, bool sorted) {
+                        double *ov, int *nz, bool sorted, bool rw) {
   if (!nrows) return;
-  if (sorted) launch_fill_t<T, WPB, true>(nrows, rows, a, b, base, oci, ov, nz);
-  else launch_fill_t<T, WPB, false>(nrows, rows, a, b, base, oci, ov, nz);
+  if (sorted && rw) launch_fill_t<T, WPB, true, true>(nrows, rows, a, b, base, oci, ov, nz);
+  else if (sorted) launch_fill_t<T, WPB, true, false>(nrows, rows, a, b, base, oci, ov, nz);
+  else if (rw) launch_fill_t<T, WPB, false, true>(nrows, rows, a, b, base, oci, ov, nz);
+  else launch_fill_t<T, WPB, false, false>(nrows, rows, a, b, base, oci, ov, nz);
 }
 
 static bool fill_sparse_tables() {  // MG_SPGEMM_SPARSE=0: load factor 1/2 in every bin (A/B)
@@ -456,7 +517,17 @@ static bool fill_sparse_tables() {  // MG_SPGEMM_SPARSE=0: load factor 1/2 in ev
   return on;
 }
 
-Csr spgemm(const Csr &a, const Csr &b, bool sorted) {
+// MG_SPGEMM_ROWWISE=0 disables the one-B-row windows (A/B)
+static bool rowwise_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_SPGEMM_ROWWISE");
+    on = !(e && *e == '0');
+  }
+  return on;
+}
+
+Csr spgemm(const Csr &a, const Csr &b, bool sorted, bool b_unique) {
   if (a.b != 1 || b.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spgemm: scalar CSR only");
   if (a.nc != b.nr) throw MgError(MG_ERR_DIM_MISMATCH, "matmul: inner dimensions differ");
   int m = a.nr;
@@ -466,6 +537,9 @@ Csr spgemm(const Csr &a, const Csr &b, bool sorted) {
     dzero(c.rp.p, sizeof(int) * ((size_t)m + 1));
     return c;
   }
+  // one-B-row windows when B's rows are long enough to fill most of a window and
+  // known to hold distinct columns (a product this library formed)
+  const bool rw = b_unique && rowwise_enabled() && b.nr && (double)b.nnz / b.nr >= 20.0;
   DBuf<int> ub(m), cnt(m), nz(m);
   MG_ROWGROUP_LAUNCH(k_row_ub, m, a.nnz, m, a.rp.p, a.ci.p, b.rp.p, ub.p);
   check_launch("row_ub");
@@ -473,7 +547,7 @@ Csr spgemm(const Csr &a, const Csr &b, bool sorted) {
     // count pass, tables sized by the product count (all keys could be distinct)
     RowBins bins;
     bins.build(ub.p, m, 1);
-#define CB(k, T, W) launch_count<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, cnt.p)
+#define CB(k, T, W) launch_count<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, cnt.p, rw)
     CB(0, 64, 8);
     CB(1, 128, 8);
     CB(2, 256, 8);
@@ -484,7 +558,8 @@ Csr spgemm(const Csr &a, const Csr &b, bool sorted) {
 #undef CB
     int ng = bins.cnt[NBIN];
     if (ng) {
-      k_spgemm_count_g<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
+      auto kern = rw ? k_spgemm_count_g<true> : k_spgemm_count_g<false>;
+      kern<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
           ng, bins.rows.p + bins.off[NBIN], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, b.rp.p, b.ci.p,
           cnt.p);
       check_launch("spgemm_count_g");
@@ -499,7 +574,7 @@ Csr spgemm(const Csr &a, const Csr &b, bool sorted) {
     RowBins bins;
     bins.build(cnt.p, m, 2);
 #define FB(k, T, W) \
-  launch_fill<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, trp.p, tci.p, tv.p, nz.p, sorted)
+  launch_fill<T, W>(bins.cnt[k], bins.rows.p + bins.off[k], a, b, trp.p, tci.p, tv.p, nz.p, sorted, rw)
     if (fill_sparse_tables()) {
       // load factor <= 1/4 for the two small bins (shorter probe runs: fill 9.7 ->
       // 8.8 ms and 11.1 -> 9.5 ms at 128^3); larger tables cost more in occupancy
@@ -519,7 +594,8 @@ Csr spgemm(const Csr &a, const Csr &b, bool sorted) {
 #undef FB
     int ng = bins.cnt[NBIN];
     if (ng) {
-      auto kern = sorted ? k_spgemm_fill_g<true> : k_spgemm_fill_g<false>;
+      auto kern = sorted ? (rw ? k_spgemm_fill_g<true, true> : k_spgemm_fill_g<true, false>)
+                         : (rw ? k_spgemm_fill_g<false, true> : k_spgemm_fill_g<false, false>);
       kern<<<grid_for((int64_t)ng * 32, 128), 128, 0, stream()>>>(
           ng, bins.rows.p + bins.off[NBIN], bins.goff.p, bins.gsize.p, bins.pool.p, a.rp.p, a.ci.p, a.v.p, b.rp.p,
           b.ci.p, b.v.p, trp.p, tci.p, tv.p, nz.p);
