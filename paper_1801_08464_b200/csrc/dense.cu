@@ -155,34 +155,35 @@ __global__ void k_aug_extract(const double *aug, double *inv, int n) {
 // the small MGR F blocks are diagonally dominant in practice).
 constexpr int BGJ = 32;
 
-// the diagonal block D = M_KK inverted in place by one warp: lane c holds column c
-// in registers; step k broadcasts column k (32 shuffles) and updates every column
-__global__ void __launch_bounds__(32) k_bgj_diag(double *m, int n, int k0, double *dinv, int *bad) {
-  const int c = threadIdx.x;
+// the diagonal block D = M_KK inverted in place by one CTA of 32 x 32 threads, one
+// element each, in shared memory: step k reads its pivot row / column entries, syncs,
+// writes (the same arithmetic as a column-per-lane register form: rks = D[k][c] / p,
+// D[i][c] -= D[i][k] * rks), 2 barriers per step instead of 32 dependent shuffles
+__global__ void __launch_bounds__(BGJ * BGJ) k_bgj_diag(double *m, int n, int k0, double *dinv, int *bad) {
+  __shared__ double a[BGJ][BGJ + 1];
+  const int c = threadIdx.x, r = threadIdx.y;
   const int nb = min(BGJ, n - k0);
-  double col[BGJ];
-#pragma unroll
-  for (int i = 0; i < BGJ; ++i)
-    col[i] = (i < nb && c < nb) ? m[(int64_t)(k0 + i) * n + k0 + c] : (i == c ? 1.0 : 0.0);
-#pragma unroll
+  a[r][c] = (r < nb && c < nb) ? m[(int64_t)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
+  __syncthreads();
+#pragma unroll 1
   for (int k = 0; k < BGJ; ++k) {
-    const double rk = col[k];  // D[k][c]
-    double amax = fabs(rk);
-    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    const double p = __shfl_sync(0xffffffffu, rk, k);
-    if (c == 0 && (!(fabs(p) > 1e-10 * amax) || !(fabs(p) > 1e-300))) atomicCAS(bad, -1, k0 + k);
+    const double rk = a[k][c];  // D[k][c]
+    const double ci = a[r][k];  // D[r][k]
+    const double p = a[k][k];
+    if (r == k) {  // warp k holds row k: the pivot test against the row's largest entry
+      double amax = fabs(rk);
+      for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (c == 0 && (!(fabs(p) > 1e-10 * amax) || !(fabs(p) > 1e-300))) atomicCAS(bad, -1, k0 + k);
+    }
+    __syncthreads();
     const double ip = 1.0 / p;
     const double rks = rk * ip;
-#pragma unroll
-    for (int i = 0; i < BGJ; ++i) {
-      const double ci = __shfl_sync(0xffffffffu, col[i], k);  // D[i][k]
-      if (c == k) col[i] = (i == k) ? ip : -ci * ip;
-      else if (i == k) col[i] = rks;
-      else col[i] = col[i] - ci * rks;
-    }
+    if (c == k) a[r][k] = (r == k) ? ip : -ci * ip;
+    else if (r == k) a[k][c] = rks;
+    else a[r][c] = a[r][c] - ci * rks;
+    __syncthreads();
   }
-#pragma unroll
-  for (int i = 0; i < BGJ; ++i) dinv[i * BGJ + c] = col[i];
+  dinv[r * BGJ + c] = a[r][c];
 }
 
 // M_Kj <- D M_Kj for j outside K: one thread per column j (coalesced across j)
@@ -282,7 +283,7 @@ static int blocked_gj(const double *a_dev, double *inv_dev, int n) {
   MG_CUDA(cudaMemcpyAsync(inv_dev, a_dev, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, stream()));
   const dim3 tiles((n + 63) / 64, (n + 63) / 64);
   for (int k0 = 0; k0 < n; k0 += BGJ) {
-    k_bgj_diag<<<1, 32, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
+    k_bgj_diag<<<1, dim3(BGJ, BGJ), 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
     k_bgj_rowpanel<<<(n + 255) / 256, 256, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
     k_bgj_update<<<tiles, 256, 0, stream()>>>(inv_dev, n, k0, bad.p);
     k_bgj_colpanel<<<(n + 255) / 256, 256, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
