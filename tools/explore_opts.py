@@ -3,7 +3,8 @@ and hierarchy shapes for variants of the AMG options and the MGR plan.
 
     python tools/explore_opts.py CFG EDGE 'label:key=val,key=val' ...
 keys: any AmgOptions field (e.g. coarse_size_cutoff=2000), gr=1 (global block
-relaxation on every MGR level), frpre / frpost (F-relaxation sweeps).
+relaxation on every MGR level), frpre / frpost (F-relaxation AMG sweeps),
+fr=jacobi|gauss_seidel|amg and frsweeps=N (the F-relaxation kind, mgr.py:159-209).
 """
 import os
 import statistics
@@ -20,15 +21,21 @@ def run(ctx, s, label, kv, reps=3, warm=2):
     amg_kw = dict(pipeline.DEFAULT_AMG)
     fr_kw = dict(pipeline.DEFAULT_FRELAX)
     gr = False
+    fr_kind, fr_sweeps = "amg", 1
     for k, v in kv.items():
         if k == "gr":
             gr = bool(int(v))
+        elif k == "fr":
+            fr_kind = v
+        elif k == "frsweeps":
+            fr_sweeps = int(v)
         elif k in ("frpre", "frpost"):
             fr_kw["pre" if k == "frpre" else "post"] = int(v)
         else:
             amg_kw[k] = type(pipeline.DEFAULT_AMG.get(k, 0))(v) if k in pipeline.DEFAULT_AMG else int(v)
     solver = pipeline.SyntheticSolver(rel_tol=1e-8, ctx=ctx, amg_opts=pipeline.default_amg_options(**amg_kw),
-                                      frelax=FRelax("amg", **fr_kw), global_relax=gr)
+                                      frelax=FRelax("amg", **fr_kw) if fr_kind == "amg" else FRelax(fr_kind, sweeps=fr_sweeps),
+                                      global_relax=gr)
     solver.upload(s)
     rows = []
     for r in range(warm + reps):
@@ -42,7 +49,8 @@ def run(ctx, s, label, kv, reps=3, warm=2):
     su = statistics.median(x[0] for x in rows)
     so = statistics.median(x[1] for x in rows)
     print(f"{label:28s} its {rows[-1][2]:4d} setup {su:7.1f} solve {so:7.1f} ms  {s.n / ((su + so) / 1e3) / 1e6:6.2f} "
-          f"MDOF/s  F-AMG {h.amg(0).level_sizes()} coarse {h.amg(-1).level_sizes()}", flush=True)
+          f"MDOF/s  F-AMG {h.amg(0).level_sizes() if fr_kind == 'amg' else fr_kind} coarse {h.amg(-1).level_sizes()}",
+          flush=True)
     solver.hier.free()
     solver.a.free()
 
