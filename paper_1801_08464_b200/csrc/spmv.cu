@@ -821,6 +821,14 @@ static double sell_long_avg() {
   return v;
 }
 
+static int csr_mid_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MG_CSR_MID");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 static int csr_long_variant() {
   static int v = -1;
   if (v < 0) {
@@ -882,7 +890,15 @@ static void launch_csr(const Csr &a, XG x, Epi epi) {
   // ~26/row (F-relax A_1, 58 -> 68% of HBM), 8 x 4 for ~40-60/row, 16 x 4
   // for the ~100-150/row coarse-AMG levels (76 -> 84%)
   else if (avg <= 36) LAUNCH_AVG(8, 2);
-  else if (avg <= 72) LAUNCH_AVG(8, 4);
+  else if (avg <= 72) {
+    switch (csr_mid_variant()) {  // MG_CSR_MID (A/B of the lane split for 37-72 per row)
+      case 1: LAUNCH_AVG(16, 2); break;
+      case 2: LAUNCH_AVG(16, 4); break;
+      case 3: LAUNCH_AVG(8, 2); break;
+      case 4: LAUNCH_AVG(4, 4); break;
+      default: LAUNCH_AVG(8, 4);
+    }
+  }
   else {
     switch (csr_long_variant()) {  // MG_CSR_LONG (A/B of the lane split for > 72 per row)
       case 1: LAUNCH_AVG(16, 8); break;
