@@ -186,6 +186,7 @@ static void neutralise_all(Ctx *c) {
 }
 
 Ctx::~Ctx() {
+  if (parked_exec) cudaGraphExecDestroy(parked_exec);
   for (auto &w : workers) {
     if (!w) continue;
     cudaStreamSynchronize(w->stream);

@@ -58,6 +58,10 @@ struct Ctx {
   size_t cub_cap = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // mg_timer_start / mg_timer_stop
   cudaStream_t copy_stream = nullptr;         // mg_mat_upload_bsr_async (created on first use)
+  // the executable graph of the last freed MGR hierarchy, kept so the next
+  // hierarchy's apply graph (same topology when the level shapes repeat) is
+  // installed with cudaGraphExecUpdate instead of a fresh instantiation
+  cudaGraphExec_t parked_exec = nullptr;
   // caching allocator state (common.cu); owned by the API context, shared by
   // its worker contexts under `amu`.  Every block has a home pool (the context
   // that cudaMalloc'ed it: 0 = API context, k = worker k) and returns there

@@ -779,7 +779,10 @@ static void mgr_apply_direct(Mgr &h, const double *r, double *e, const double *c
 }
 
 void Mgr::drop_graph() {
-  if (gexec) cudaGraphExecDestroy(gexec);
+  if (!gexec) return;
+  // park it in its context for the next hierarchy's update (one slot)
+  if (gctx && !gctx->parked_exec) gctx->parked_exec = gexec;
+  else cudaGraphExecDestroy(gexec);
   gexec = nullptr;
 }
 Mgr::~Mgr() { drop_graph(); }
@@ -821,7 +824,21 @@ static bool capture_apply(Mgr &h) {
     g_ctx->launches = l0;
     return false;
   }
-  e = cudaGraphInstantiate(&h.gexec, graph, 0);
+  // a parked executable of a previous hierarchy with the same topology is updated
+  // in place (kernel parameters only), else a new one is instantiated
+  e = cudaErrorUnknown;
+  if (g_ctx->parked_exec) {
+    cudaGraphExecUpdateResultInfo info{};
+    if (cudaGraphExecUpdate(g_ctx->parked_exec, graph, &info) == cudaSuccess) {
+      h.gexec = g_ctx->parked_exec;
+      e = cudaSuccess;
+    } else {
+      cudaGetLastError();
+      cudaGraphExecDestroy(g_ctx->parked_exec);
+    }
+    g_ctx->parked_exec = nullptr;
+  }
+  if (e != cudaSuccess) e = cudaGraphInstantiate(&h.gexec, graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -830,6 +847,7 @@ static bool capture_apply(Mgr &h) {
     return false;
   }
   h.graph_kernels = g_ctx->launches - l0;
+  h.gctx = g_ctx;
   g_ctx->launches = l0;
   return true;
 }

@@ -103,6 +103,7 @@ struct Mgr {
   // gout.  Input: with a prescale, read through the device pointer slot in_slot
   // (set by a one-thread kernel before each replay: no copy); else copied into gin.
   cudaGraphExec_t gexec = nullptr;
+  Ctx *gctx = nullptr;          // context whose stream the graph was captured on
   DBuf<double> gin, gout;
   DBuf<const double *> in_slot;
   int64_t graph_kernels = 0;

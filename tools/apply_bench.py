@@ -30,6 +30,17 @@ def main():
     ctx.call("mg_dev_alloc", 8 * n, ctypes.byref(e))
     rh = np.random.default_rng(0).standard_normal(n)
     ctx.call("mg_memcpy_h2d", r, _lib.ptr(rh), 8 * n)
+    import time
+    ctx.sync()
+    t0 = time.perf_counter()
+    ctx.call("mg_mgr_apply_dev", solver.hier.h, r, e)  # first apply: graph capture + instantiate
+    ctx.sync()
+    t1 = time.perf_counter()
+    ctx.call("mg_mgr_apply_dev", solver.hier.h, r, e)
+    ctx.sync()
+    t2 = time.perf_counter()
+    print(f"first apply (capture + instantiate + run) {1e3 * (t1 - t0):.2f} ms, second {1e3 * (t2 - t1):.2f} ms",
+          flush=True)
     for _ in range(5):
         ctx.call("mg_mgr_apply_dev", solver.hier.h, r, e)
     ctx.sync()
