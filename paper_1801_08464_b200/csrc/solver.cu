@@ -838,8 +838,11 @@ static bool capture_apply(Mgr &h) {
     }
     g_ctx->parked_exec = nullptr;
   }
+  const bool updated = e == cudaSuccess;
   if (e != cudaSuccess) e = cudaGraphInstantiate(&h.gexec, graph, 0);
   cudaGraphDestroy(graph);
+  static const bool gtrace = getenv("MG_GRAPH_TRACE") != nullptr;
+  if (gtrace) fprintf(stderr, "[mg] MGR apply graph %s\n", updated ? "updated in place" : "instantiated");
   if (e != cudaSuccess) {
     cudaGetLastError();
     h.gexec = nullptr;

@@ -219,6 +219,21 @@ def test_repeated_setup_and_solve_bitwise_deterministic(gpu):
     np.testing.assert_array_equal(r1.x, r3.x)
 
 
+def test_graph_reuse_across_systems(gpu):
+    """A solver reused on a new system of the same shape installs the new MGR apply
+    graph into the previous hierarchy's parked executable (cudaGraphExecUpdate,
+    solver.cu capture_apply): the solution must equal a fresh solver's bit for bit,
+    for a system solved after another one with different values."""
+    s1 = synth.make_config(3, 40, seed=11)
+    s2 = synth.make_config(3, 40, seed=12)
+    sol = gpipe.SyntheticSolver(rel_tol=1e-10)
+    sol.solve_system(s1)
+    r_reused, _ = sol.solve_system(s2)
+    r_fresh, _ = gpipe.SyntheticSolver(rel_tol=1e-10).solve_system(s2)
+    assert r_reused.converged and r_reused.iterations == r_fresh.iterations
+    np.testing.assert_array_equal(r_reused.x, r_fresh.x)
+
+
 def test_dense_inverse_needs_pivoting(gpu):
     """IDEAL R/P and exact F / coarse solves on blocks with zero diagonals (n > 256):
     the unpivoted blocked Gauss-Jordan rejects the pivot and the partially pivoted
