@@ -240,6 +240,125 @@ __global__ void __launch_bounds__(256) k_sell(int nr, const int *__restrict__ sp
   epi(row, sum);
 }
 
+// ---- SELL-32, u8 codes, the matrix streamed by bulk copies (TMA 1-D) ----------
+// A CTA of 256 threads owns 8 consecutive slices (256 rows).  Stage t carries
+// entries [4t, 4t+4) of all 8 slices: per slice one 1 KB copy of the values and
+// one 128 B copy of the packed codes (cp.async.bulk into shared memory, completion
+// counted on the stage's mbarrier).  D stages are in flight; thread 0 refills a
+// stage after the CTA-wide barrier that ends its consumption.  Each thread sums its
+// row in entry order from shared memory, so results equal k_sell's bit for bit.
+// (The streamed loads no longer occupy registers or load slots: the x gathers issue
+// as soon as a stage lands.)  MG_SELL_TMA=1 selects it for u8-coded, unpermuted
+// SELL operators of <= 64 entries per row.
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Per-warp pipelines: warp w of the CTA streams its own slice; stage t = entries
+// [E t, E t + E) (one E x 32-value copy and one E x 8-byte code copy); TMA_D stages
+// in flight per warp; lane 0 refills a stage after a __syncwarp, so slices of
+// different lengths never wait for each other.
+template <class Epi, int TMA_D, int TMA_E, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_sell_tma(int nr, const int *__restrict__ sptr, const int *__restrict__ rlen,
+                                                  const unsigned *__restrict__ codes, const int *__restrict__ dict,
+                                                  unsigned long long mul, const double *__restrict__ v, XPlain x,
+                                                  Epi epi) {
+  __shared__ int tbl[256];
+  __shared__ __align__(128) double sv[WPB][TMA_D][TMA_E * 32];
+  __shared__ __align__(128) unsigned sc[WPB][TMA_D][TMA_E * 8];
+  __shared__ __align__(8) uint64_t full[WPB][TMA_D];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int ns_total = (nr + 31) >> 5;
+  const int s = blockIdx.x * WPB + w;
+  if (lane == 0) {
+    for (int d = 0; d < TMA_D; ++d) mbar_init(&full[w][d], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  PDL_ENTRY();
+  for (int i = tid; i < 256; i += blockDim.x) tbl[i] = __ldg(dict + i);
+  __syncthreads();
+  const int sb = s < ns_total ? __ldg(sptr + s) : 0;
+  const int sl = s < ns_total ? (__ldg(sptr + s + 1) - sb) >> 5 : 0;  // entries per row slot (multiple of 4)
+  const int nst = (sl + TMA_E - 1) / TMA_E;
+  auto issue = [&](int t) {
+    const int b = t % TMA_D;
+    const int e = min(TMA_E, sl - TMA_E * t);  // entries in this stage (a multiple of 4)
+    mbar_expect_tx(&full[w][b], (unsigned)e * 32u * 9u);
+    bulk_g2s(sv[w][b], v + sb + 32 * TMA_E * t, (unsigned)e * 256u, &full[w][b]);
+    bulk_g2s(sc[w][b], codes + (sb >> 2) + 8 * TMA_E * t, (unsigned)e * 32u, &full[w][b]);
+  };
+  if (lane == 0)
+    for (int t = 0; t < TMA_D && t < nst; ++t) issue(t);
+  const int row = s * 32 + lane;
+  const bool live = row < nr;
+  const int len = live ? __ldg(rlen + row) : 0;
+  const int anc = sell_anchor(row, mul);
+  double sum = 0.0;
+  for (int t = 0; t < nst; ++t) {
+    const int b = t % TMA_D;
+    const int k0 = TMA_E * t;
+    if (k0 < len) {
+      const unsigned par = (unsigned)((t / TMA_D) & 1);
+      unsigned spins = 0;
+      while (!mbar_try_wait(&full[w][b], par))
+        if (++spins > (1u << 28)) __trap();  // a lost stage must fail loudly, never hang
+#pragma unroll
+      for (int q = 0; q < TMA_E / 4; ++q) {
+        const int k = k0 + 4 * q;
+        if (k < len) {
+          const unsigned cw = sc[w][b][q * 32 + lane];
+          const int m = len - k;
+          double vv[4];
+          int cc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            vv[u] = sv[w][b][(4 * q + u) * 32 + lane];
+            cc[u] = anc + tbl[(cw >> (8 * u)) & 255u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < m) sum += vv[u] * x(cc[u]);
+        }
+      }
+    }
+    __syncwarp();  // every lane is done with stage buffer b
+    if (lane == 0 && t + TMA_D < nst) issue(t + TMA_D);
+  }
+  if (live) epi(row, sum);
+}
+
+static int sell_tma() {  // MG_SELL_TMA=1/2/3: (stages, entries) = (4, 4) / (3, 8) / (2, 16); 0 off
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("MG_SELL_TMA");
+    on = e ? atoi(e) : 0;
+  }
+  return on;
+}
+
 // per slice: max row length (warp per slice); Q rounds the slice length up to a
 // multiple of Q entries (4 for the scalar SELL copy: whole code words)
 __global__ void k_sell_len(int nr, int ns, const int *rp, const int *perm, int *rlen, int *slen, int q) {
@@ -867,6 +986,20 @@ static void launch_csr(const Csr &a, XG x, Epi epi) {
       launch_pdl(k_sell<UNR, IK, false, Epi, XG>, grid_for(a.nr, T), T, 0, a.nr, pl.sptr.p, pl.rlen.p,         \
                  (const int *)pl.perm.p, ci, pl.dict.p, pl.mul, pl.sv.p, x, epi);                              \
   } while (0)
+    if (pl.ik == 1 && !pl.perm.p && avg >= 24 && avg <= sell_long_avg() && sell_tma()) {
+      const int vtma = sell_tma();
+      if (vtma == 1)
+        launch_pdl(k_sell_tma<Epi, 4, 4, 8>, grid_for(a.nr, 256), 256, 0, a.nr, pl.sptr.p, pl.rlen.p,
+                   (const unsigned *)pl.scode.p, pl.dict.p, pl.mul, pl.sv.p, x, epi);
+      else if (vtma == 2)
+        launch_pdl(k_sell_tma<Epi, 3, 8, 4>, grid_for(a.nr, 128), 128, 0, a.nr, pl.sptr.p, pl.rlen.p,
+                   (const unsigned *)pl.scode.p, pl.dict.p, pl.mul, pl.sv.p, x, epi);
+      else
+        launch_pdl(k_sell_tma<Epi, 2, 16, 4>, grid_for(a.nr, 128), 128, 0, a.nr, pl.sptr.p, pl.rlen.p,
+                   (const unsigned *)pl.scode.p, pl.dict.p, pl.mul, pl.sv.p, x, epi);
+      check_launch("sell tma spmv");
+      return;
+    }
     if (avg > sell_long_avg()) {
       if (pl.ik == 1) LAUNCH_SELL(8, 128, 1);
       else if (pl.ik == 2) LAUNCH_SELL(8, 128, 2);
