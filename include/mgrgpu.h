@@ -59,6 +59,13 @@ int mg_mat_upload_csr(mg_ctx *ctx, int nrows, int ncols, const int32_t *indptr,
 /* block CSR: nbrows block rows, b x b row-major blocks, sorted block columns */
 int mg_mat_upload_bsr(mg_ctx *ctx, int nbrows, int nbcols, int b, const int32_t *rowptr,
                       const int32_t *colind, const double *vals, mg_mat **out);
+/* the reference's BlockSystem matrix (assembly.py:95-120: scalar CSR over the
+   variable-major unknowns u = var * N + cell, N = n / b) converted on the device
+   into the cell-major b x b block CSR the block kernels use (SURVEY.md §8(b)
+   mat_upload_csr_varmajor); block positions no entry fills are explicit zeros.
+   Vectors for it are cell-major: x_cell[cell * b + var] = x_var[var * N + cell]. */
+int mg_mat_upload_csr_varmajor(mg_ctx *ctx, int n, int b, const int32_t *indptr, const int32_t *indices,
+                               const double *vals, mg_mat **out);
 /* mg_mat_upload_bsr without the host wait: the copies run on the context's
    copy stream and overlap whatever the context is computing; the first call
    that uses the matrix (or mg_mat_free) orders the context stream after them.

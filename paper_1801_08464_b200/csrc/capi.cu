@@ -198,6 +198,18 @@ int mg_mat_upload_bsr(mg_ctx *ctx, int nbrows, int nbcols, int b, const int32_t 
   });
 }
 
+int mg_mat_upload_csr_varmajor(mg_ctx *ctx, int n, int b, const int32_t *indptr, const int32_t *indices,
+                               const double *vals, mg_mat **out) {
+  return guard(ctx, [&] {
+    if (b < 1 || b > 3) throw MgError(MG_ERR_UNSUPPORTED, "block size must be 1, 2 or 3");
+    if (n < 0 || n % b) throw MgError(MG_ERR_DIM_MISMATCH, "variable-major matrix: n must be b * cells");
+    Csr scalar = upload_csr(n, n, 1, indptr, indices, vals);
+    auto *m = new mg_mat();
+    try { m->m = csr_varmajor_to_bsr(scalar, b); } catch (...) { delete m; throw; }
+    *out = m;
+  });
+}
+
 int mg_mat_upload_bsr_async(mg_ctx *ctx, int nbrows, int nbcols, int b, const int32_t *rowptr,
                             const int32_t *colind, const double *vals, mg_mat **out) {
   return guard(ctx, [&] {

@@ -10,6 +10,8 @@ namespace mg {
 // b_unique: B's rows hold distinct columns (a product formed here), enabling the
 // conflict-free one-B-row windows for long B rows
 Csr spgemm(const Csr &a, const Csr &b, bool sorted = true, bool b_unique = false);
+// variable-major scalar CSR (u = var * N + cell) -> cell-major b x b block CSR
+Csr csr_varmajor_to_bsr(const Csr &a, int b);
 // A^T with ascending columns per row
 Csr transpose(const Csr &a);
 // rows_dev: nr source rows (sorted); cmap_dev: column map (source col -> new col or -1)

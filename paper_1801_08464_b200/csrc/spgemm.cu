@@ -645,6 +645,77 @@ __global__ void k_permute_entries(int64_t nnz, const int *perm, const int *rid, 
   }
 }
 
+// ---- variable-major scalar CSR -> cell-major block CSR ------------------------
+// SURVEY.md §8(b) mat_upload_csr_varmajor: the reference's BlockSystem matrix is
+// scalar CSR over unknowns u = var * N + cell (assembly.py:95-120); the block
+// kernels want block rows = cells, b x b row-major blocks, sorted block columns.
+// Entry (r, c) goes to block (r % N, c % N) at (r / N, c / N); positions no entry
+// fills are explicit zeros.  Keys (cell_r * N + cell_c) radix-sorted with the entry
+// ids, run heads give the blocks.
+__global__ void k_vm_keys(int64_t nnz, int N, const int *rid, const int *ci, int64_t *key, int *idx) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
+    key[q] = (int64_t)(rid[q] % N) * N + (ci[q] % N);
+    idx[q] = (int)q;
+  }
+}
+__global__ void k_vm_heads(int64_t nnz, const int64_t *key, int *head) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    head[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
+}
+__global__ void k_vm_fill(int64_t nnz, int N, int b, const int64_t *key, const int *head, const int *seg,
+                          const int *idx, const int *rid, const int *ci, const double *v, int *bcol, int *bcnt,
+                          double *bv) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+    const int blk = seg[p] + head[p] - 1;  // inclusive run index
+    const int q = idx[p];
+    if (head[p]) {
+      bcol[blk] = (int)(key[p] % N);
+      atomicAdd(&bcnt[key[p] / N], 1);
+    }
+    bv[(int64_t)blk * b * b + (rid[q] / N) * b + ci[q] / N] = v[q];
+  }
+}
+
+Csr csr_varmajor_to_bsr(const Csr &a, int b) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "csr_varmajor_to_bsr: scalar CSR required");
+  if (b < 1 || b > 3) throw MgError(MG_ERR_UNSUPPORTED, "block size must be 1, 2 or 3");
+  if (a.nr != a.nc || a.nr % b) throw MgError(MG_ERR_DIM_MISMATCH, "variable-major matrix: n must be b * cells");
+  const int N = a.nr / b;
+  const int64_t nnz = a.nnz;
+  Csr c;
+  if (nnz == 0) {
+    c.alloc(N, N, 0, b);
+    dzero(c.rp.p, sizeof(int) * ((size_t)N + 1));
+    return c;
+  }
+  DBuf<int> rid((size_t)nnz), idx((size_t)nnz), idx_s((size_t)nnz), head((size_t)nnz), seg((size_t)nnz + 1);
+  DBuf<int64_t> key((size_t)nnz), key_s((size_t)nnz);
+  MG_ROWGROUP_LAUNCH(k_row_ids, a.nr, a.nnz, a.nr, a.rp.p, rid.p);
+  check_launch("row_ids");
+  const int g = grid_for(nnz, 256, g_ctx->num_sms * 8);
+  k_vm_keys<<<g, 256, 0, stream()>>>(nnz, N, rid.p, a.ci.p, key.p, idx.p);
+  check_launch("vm_keys");
+  int bits = 1;
+  while (bits < 63 && ((int64_t)1 << bits) < (int64_t)N * N) ++bits;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key_s.p, idx.p, idx_s.p, (int)nnz, 0, bits, stream());
+  void *tmp = cub_scratch(tb);
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key.p, key_s.p, idx.p, idx_s.p, (int)nnz, 0, bits, stream()));
+  count_launch(4);
+  k_vm_heads<<<g, 256, 0, stream()>>>(nnz, key_s.p, head.p);
+  check_launch("vm_heads");
+  const int64_t nblk = exclusive_scan_i32_to_i32(head.p, seg.p, (int)nnz);
+  c.alloc(N, N, nblk, b);
+  DBuf<int> bcnt((size_t)N + 1);
+  dzero(bcnt.p, sizeof(int) * ((size_t)N + 1));
+  dzero(c.v.p, sizeof(double) * (size_t)nblk * b * b);
+  k_vm_fill<<<g, 256, 0, stream()>>>(nnz, N, b, key_s.p, head.p, seg.p, idx_s.p, rid.p, a.ci.p, a.v.p, c.ci.p,
+                                     bcnt.p, c.v.p);
+  check_launch("vm_fill");
+  exclusive_scan_i32_to_i32(bcnt.p, c.rp.p, N);
+  return c;
+}
+
 Csr transpose(const Csr &a) {
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "transpose: scalar CSR only");
   Csr t;

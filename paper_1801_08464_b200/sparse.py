@@ -56,6 +56,19 @@ class DeviceMatrix:
         return cls(ctx, h, (rp, ci, blocks) if asynchronous else None)
 
     @classmethod
+    def from_csr_varmajor(cls, indptr, indices, data, b, ctx=None):
+        """The reference's variable-major scalar CSR (unknown var * N + cell,
+        assembly.py:95-120) as the cell-major b x b block CSR the block kernels
+        use (mg_mat_upload_csr_varmajor; conversion on the device).  Vectors for
+        the result are cell-major: see to_cell_major / to_var_major."""
+        ctx = ctx or _lib.ctx()
+        ip, ix, dv = _lib.i32(indptr), _lib.i32(indices), _lib.f64(data)
+        h = _lib.P()
+        ctx.call("mg_mat_upload_csr_varmajor", int(ip.size - 1), int(b), _lib.ptr(ip), _lib.ptr(ix), _lib.ptr(dv),
+                 _lib.ctypes.byref(h))
+        return cls(ctx, h)
+
+    @classmethod
     def from_host(cls, a, ctx=None):
         if isinstance(a, DeviceMatrix):
             return a
@@ -262,3 +275,15 @@ def write_matrix_market(path, a, comment=""):
     import scipy.io
     m = a.to_scipy() if isinstance(a, DeviceMatrix) else (a.m if hasattr(a, "m") else a)
     scipy.io.mmwrite(path, m.tocoo(), comment=comment)
+
+
+def to_cell_major(v, b):
+    """x_cell[cell * b + var] = x_var[var * N + cell]"""
+    v = np.asarray(v)
+    return np.ascontiguousarray(v.reshape(b, -1).T).reshape(-1)
+
+
+def to_var_major(v, b):
+    """inverse of to_cell_major"""
+    v = np.asarray(v)
+    return np.ascontiguousarray(v.reshape(-1, b).T).reshape(-1)

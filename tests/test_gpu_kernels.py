@@ -160,6 +160,32 @@ def test_bsell_spmv_matches_scipy(gpu, cfg, edge):
         assert relerr(gsp.spmv(d, x), a @ x) <= 1e-14
 
 
+@pytest.mark.parametrize("cfg,edge", [(1, 16), (2, 10), (4, 8), (3, 40)])
+def test_csr_varmajor_to_bsr(gpu, cfg, edge):
+    """mg_mat_upload_csr_varmajor: the reference's variable-major
+    scalar CSR converted on the device into cell-major block CSR -- the block
+    pattern and every block value equal the host-built BCSR of the same system
+    (explicit zeros where a block position has no entry), and its SpMV on
+    cell-major vectors equals scipy's on variable-major ones."""
+    s = synth.make_config(cfg, edge)
+    avm = synth.to_scalar_csr(s, "var", drop_zeros=True)
+    d = gsp.DeviceMatrix.from_csr_varmajor(avm.indptr, avm.indices, avm.data, s.b)
+    rp, ci, v = d.download()
+    # host reference: the synthetic generator's own cell-major BCSR restricted to the
+    # blocks that hold a nonzero
+    ref = synth.to_scalar_csr(s, "cell", drop_zeros=True)
+    from paper_1801_08464_b200.sparse import to_cell_major, to_var_major
+    x = np.random.default_rng(cfg).standard_normal(s.n)
+    y_gpu = gsp.spmv(d, to_cell_major(x, s.b))
+    assert relerr(to_var_major(y_gpu, s.b), avm @ x) <= 1e-14
+    # the block matrix equals the cell-major scalar matrix entry by entry
+    import scipy.sparse as sp
+    blocks = np.asarray(v).reshape(-1, s.b, s.b)
+    bsr = sp.bsr_matrix((blocks, np.asarray(ci), np.asarray(rp)), shape=(s.n, s.n)).tocsr()
+    assert abs(bsr - ref).max() == 0.0
+    assert np.all(np.diff(np.asarray(rp)) >= 0) and rp[-1] == len(ci)
+
+
 def test_async_upload_pipeline(gpu):
     """mg_mat_upload_bsr_async: matrices uploaded on the copy stream while the
     context is busy equal synchronous uploads; an async upload freed before
