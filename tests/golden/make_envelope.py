@@ -1,6 +1,6 @@
 """Oracle self-perturbation envelopes (GMRES iteration counts) for the parity tests.
 
-    python tests/golden/make_envelope.py [--procs P] [--only sweep|full]
+    python tests/golden/make_envelope.py [--procs P] [--only sweep|full] [--full-cases cfg:edge:rtol,...]
 
 For each case the CPU oracle (oracle/pipeline.py: the reference's MGR + GMRES
 restated, PMIS / extended+i / L1 AMG in the amg_mod seam) is run unperturbed and
@@ -37,7 +37,7 @@ SWEEP = ([(3, e, 1e-10, None) for e in range(8, 21)] + [(4, e, 1e-10, None) for 
          + [(1, 32, 1e-10, None), (2, 32, 1e-10, None), (3, 32, 1e-10, None)]
          + [(3, e, 1e-10, 50) for e in range(8, 21)] + [(4, e, 1e-10, 50) for e in range(5, 13)])
 FULL = [(1, 64, 1e-10, None), (2, 64, 1e-10, None), (3, 128, 1e-10, None), (3, 128, 1e-8, None),
-        (4, 48, 1e-10, None)]
+        (4, 48, 1e-10, None), (3, 64, 1e-8, None), (3, 96, 1e-8, None), (4, 64, 1e-8, None), (4, 96, 1e-8, None)]
 
 
 def key(cfg, edge, rtol, cut=None):
@@ -92,6 +92,12 @@ def main():
         tasks += tasks_for(SWEEP, 4, 48, 13)
     if only in (None, "full"):
         tasks = tasks_for(FULL, 4, 4, 1) + tasks  # largest first
+    if "--full-cases" in sys.argv:  # cfg:edge:rtol,... (a subset of FULL, re-run)
+        sel = []
+        for c in sys.argv[sys.argv.index("--full-cases") + 1].split(","):
+            f = c.split(":")
+            sel.append((int(f[0]), int(f[1]), float(f[2]), None))
+        tasks = tasks_for(sel, 4, 4, 1) + tasks
     data = json.load(open(OUT)) if os.path.exists(OUT) else {}
     fresh = set()
     with mp.get_context("spawn").Pool(procs) as pool:

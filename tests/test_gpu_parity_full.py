@@ -30,9 +30,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 ENVELOPE = json.load(open(os.path.join(HERE, "golden", "envelope.json")))
 
-# (config, edge, rtol): configs 1 / 2 / 3 at their stated sizes; config 4 at 48^3
-# (its stated 96^3 needs ~280 oracle iterations, too long for the GPU test step)
-CASES = [(1, 64, 1e-10), (2, 64, 1e-10), (3, 128, 1e-10), (3, 128, 1e-8), (4, 48, 1e-10)]
+# (config, edge, rtol): configs 1 / 2 / 3 at their stated sizes (rtol 1e-10 and the
+# bench's 1e-8), config 4 at 48^3 (rtol 1e-10) and at its stated 96^3 (rtol 1e-8, ~200
+# iterations); config 3 at 64^3 / 96^3 and config 4 at 64^3 (rtol 1e-8) in between
+CASES = [(1, 64, 1e-10), (2, 64, 1e-10), (3, 128, 1e-10), (3, 128, 1e-8), (4, 48, 1e-10),
+         (3, 64, 1e-8), (3, 96, 1e-8), (4, 64, 1e-8), (4, 96, 1e-8)]
 
 
 def _oracle_job(cfg, edge, rtol):
