@@ -196,6 +196,10 @@ typedef struct {
   uint64_t seed;           /* PMIS measure seed */
 } mg_amg_opts;
 
+/* strength_graph (amg.py:88-103): int8 mask over every stored entry of A (1 = strong:
+   cand >= theta * rowmax and rowmax > 0, cand = -a_ij for negative off-diagonals,
+   |a_ij| in rows without one; the diagonal is never strong); n_strong may be NULL */
+int mg_strength(mg_ctx *ctx, const mg_mat *a, double theta, int8_t *mask, int64_t *n_strong);
 int mg_amg_setup(mg_ctx *ctx, const mg_mat *a, const mg_amg_opts *opts, mg_amg **out);
 /* one V(pre,post) cycle from x0 (NULL = zero), amg.py:370-378 */
 int mg_amg_vcycle(mg_ctx *ctx, mg_amg *h, const double *b, const double *x0, double *x);

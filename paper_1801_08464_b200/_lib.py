@@ -58,6 +58,7 @@ _SIGS = {
     "mg_mat_upload_bsr": [P, c_int, c_int, c_int, P, P, P, ctypes.POINTER(P)],
     "mg_mat_upload_bsr_async": [P, c_int, c_int, c_int, P, P, P, ctypes.POINTER(P)],
     "mg_mat_upload_csr_varmajor": [P, c_int, c_int, P, P, P, ctypes.POINTER(P)],
+    "mg_strength": [P, P, ctypes.c_double, P, P],
     "mg_mat_info": [P, P, ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int64),
                     ctypes.POINTER(c_int)],
     "mg_mat_download": [P, P, P, P, P],

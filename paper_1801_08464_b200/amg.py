@@ -167,6 +167,20 @@ class AmgHierarchy:
             pass
 
 
+def strength_graph(a, theta: float):
+    """Strong-connection mask aligned with a's stored entries (amg.py:88-103), on
+    the device (mg_strength): returned as the reference does, a scipy CSR of int8
+    with a's own pattern."""
+    import scipy.sparse as sp
+    from .sparse import DeviceMatrix
+    d = DeviceMatrix.from_host(a)
+    ip, ix, _ = d.download()
+    mask = np.zeros(ix.size, dtype=np.int8)
+    d.ctx.call("mg_strength", d.h, float(theta), _lib.ptr(mask), None)
+    n = ip.size - 1
+    return sp.csr_matrix((mask, ix, ip), shape=(n, n))
+
+
 def amg_setup(a, opts=None) -> AmgHierarchy:
     o = as_options(opts)
     d = as_device(a)

@@ -392,6 +392,18 @@ int mg_build_rp(mg_ctx *ctx, const mg_mat *a, const uint8_t *f_mask, int kind, m
   });
 }
 
+int mg_strength(mg_ctx *ctx, const mg_mat *a, double theta, int8_t *mask, int64_t *n_strong) {
+  return guard(ctx, [&] {
+    const Csr &m = C(a);
+    if (m.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "strength_graph: scalar CSR required");
+    if (!(theta > 0.0 && theta < 1.0)) throw MgError(MG_ERR_BAD_OPTION, "strength_theta must lie in (0, 1)");
+    DBuf<int8_t> s;
+    const int64_t ns = strength(m, theta, s);
+    if (m.nnz) d2h(mask, s.p, (size_t)m.nnz);
+    if (n_strong) *n_strong = ns;
+  });
+}
+
 int mg_amg_setup(mg_ctx *ctx, const mg_mat *a, const mg_amg_opts *opts, mg_amg **out) {
   return guard(ctx, [&] {
     auto h = std::make_unique<mg_amg>();

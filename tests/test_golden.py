@@ -75,6 +75,17 @@ def test_oracle_strength(nm, th):
     np.testing.assert_array_equal(oamg.strength_graph(mat(f"g5_{nm}"), th), G[f"g5_s_{nm}_{th}"])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("nm", ["poi", "ns"])
+@pytest.mark.parametrize("th", [0.25, 0.5])
+def test_gpu_strength_golden(gpu, nm, th):
+    """The device strength graph (mg_strength, amg_setup.cu k_strength) against the
+    reference's own strength_graph outputs (golden g5), entry for entry."""
+    from paper_1801_08464_b200 import amg as gamg
+    s = gamg.strength_graph(mat(f"g5_{nm}"), th)
+    np.testing.assert_array_equal(s.data, G[f"g5_s_{nm}_{th}"])
+
+
 def test_oracle_synthetic_mgr_level():
     s = synth.make_config(1, 16)
     _, ahat = obs.block_scale(s)
