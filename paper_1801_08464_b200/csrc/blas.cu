@@ -497,11 +497,12 @@ __global__ void __launch_bounds__(256) k_mdot2x_t(const double *__restrict__ V, 
 }
 
 static bool mdot2x_tiled() {  // MG_MDOT2X_TILED=0: warp-per-vector kernel (A/B)
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_MDOT2X_TILED");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on;
 }
 

@@ -211,11 +211,12 @@ TaskGroup::~TaskGroup() {
 }
 
 static bool concurrent_setup() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_CONCURRENT_SETUP");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on;
 }
 
@@ -340,11 +341,12 @@ void sync() {
 }
 
 bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_PDL");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on;
 }
 
@@ -353,11 +355,12 @@ static bool timeline_on();
 bool trace_on() {
   if (timeline_on()) return false;          // timeline mode: no synchronising trace
   if (g_ctx && g_ctx->owner) return false;  // worker threads do not trace
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_TRACE");
     on = e && *e && *e != '0';
-  }
+    return on;
+  }();
   return on;
 }
 
@@ -367,11 +370,12 @@ static std::mutex tl_mu;
 static std::vector<std::pair<double, std::string>> tl_events;
 static std::chrono::steady_clock::time_point tl_t0;
 static bool timeline_on() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_TIMELINE");
     on = e && *e == '1';
-  }
+    return on;
+  }();
   return on;
 }
 void timeline_reset() {

@@ -42,11 +42,12 @@ void prof_reset() {
   g_ctx->timing.frelax_bytes = 0.0;
 }
 static bool level_prof() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_PROF_LEVELS");
     on = e && *e == '1';
-  }
+    return on;
+  }();
   return on;
 }
 
@@ -788,11 +789,12 @@ void Mgr::drop_graph() {
 Mgr::~Mgr() { drop_graph(); }
 
 static bool graphs_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_GRAPHS");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on != 0;
 }
 

@@ -509,21 +509,23 @@ static void launch_fill(int nrows, const int *rows, const Csr &a, const Csr &b, 
 }
 
 static bool fill_sparse_tables() {  // MG_SPGEMM_SPARSE=0: load factor 1/2 in every bin (A/B)
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_SPGEMM_SPARSE");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on;
 }
 
 // MG_SPGEMM_ROWWISE=0 disables the one-B-row windows (A/B)
 static bool rowwise_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_SPGEMM_ROWWISE");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on;
 }
 

@@ -351,11 +351,12 @@ __global__ void __launch_bounds__(WPB * 32) k_sell_tma(int nr, const int *__rest
 }
 
 static int sell_tma() {  // MG_SELL_TMA=1/2/3: (stages, entries) = (4, 4) / (3, 8) / (2, 16); 0 off
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_SELL_TMA");
     on = e ? atoi(e) : 0;
-  }
+    return on;
+  }();
   return on;
 }
 
@@ -534,11 +535,12 @@ __global__ void k_code_fill_csr(int nr, const int *__restrict__ rp, const int *_
 }
 
 static int code_mode() {  // MG_SELL_CODES=0 keeps int32 columns
-  static int m = -1;
-  if (m < 0) {
+  static const int m = [] {
+    int m = -1;
     const char *e = getenv("MG_SELL_CODES");
     m = e ? atoi(e) : 1;
-  }
+    return m;
+  }();
   return m;
 }
 
@@ -598,20 +600,22 @@ static void build_codes(const Csr &a, SpmvPlan &pl, int64_t padded) {
 }
 
 static int sell_min_rows() {  // MG_SELL_MIN_ROWS: smallest operator given a SELL copy
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
+    int v = -1;
     const char *e = getenv("MG_SELL_MIN_ROWS");
     v = e ? atoi(e) : 32768;
-  }
+    return v;
+  }();
   return v;
 }
 
 static double sell_min_avg() {
-  static double v = -1.0;
-  if (v < 0) {
+  static const double v = [] {
+    double v = -1.0;
     const char *e = getenv("MG_SELL_MIN_AVG");
     v = e ? atof(e) : 3.0;
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -645,11 +649,12 @@ __global__ void __launch_bounds__(256) k_sell_sort_window(int nr, const int *__r
 // per row) 34 -> 53 us, the long per-thread row loops left without enough
 // warps to hide latency.  MG_SELL_SIGMA=<min rows>, 0 disables.
 static int sell_sigma_min_rows() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
+    int v = -1;
     const char *e = getenv("MG_SELL_SIGMA");
     v = e ? atoi(e) : 262144;
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -667,16 +672,18 @@ static void build_sell(const Csr &a, SpmvPlan &pl) {
   // short rows (where CSR lane groups are inefficient), 1.15x otherwise
   // (measured: irregular long-row coarse levels lose with SELL)
   double avg = (double)a.nnz / (a.nr ? a.nr : 1);
-  static double cap_long = -1.0;
-  if (cap_long < 0) {
+  static const double cap_long = [] {
+    double cap_long = -1.0;
     const char *e = getenv("MG_SELL_CAP_LONG");
     cap_long = e ? atof(e) : 1.15;
-  }
-  static double cap_short = -1.0;
-  if (cap_short < 0) {
+    return cap_long;
+  }();
+  static const double cap_short = [] {
+    double cap_short = -1.0;
     const char *e = getenv("MG_SELL_CAP_SHORT");
     cap_short = e ? atof(e) : 2.0;
-  }
+    return cap_short;
+  }();
   double cap = avg <= 16.0 ? cap_short : cap_long;
   // (+ the rounding of slice lengths to whole code words: at most 3 x 32 per slice)
   auto over = [&](int64_t pd) { return pd > (int64_t)(cap * (double)a.nnz) + 4096 + 96LL * ns || pd > 2000000000LL; };
@@ -921,39 +928,43 @@ static int spmv_grid(int64_t threads_needed) {
 // per row) 77 -> 85% of HBM; the short-row variant loses with it (occupancy:
 // 56 registers), A_hat 71 -> 61%.  MG_SELL_PF=0: plain unrolled loop (A/B).
 static bool sell_pf() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_SELL_PF");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on;
 }
 
 // rows longer than this (average) take the UNR = 8 SELL kernel (software pipelined
 // with MG_SELL_PF) instead of UNR = 4; MG_SELL_LONG_AVG overrides (A/B)
 static double sell_long_avg() {
-  static double v = -1.0;
-  if (v < 0) {
+  static const double v = [] {
+    double v = -1.0;
     const char *e = getenv("MG_SELL_LONG_AVG");
     v = e ? atof(e) : 64.0;
-  }
+    return v;
+  }();
   return v;
 }
 
 static int csr_mid_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
+    int v = -1;
     const char *e = getenv("MG_CSR_MID");
     v = e ? atoi(e) : 0;
-  }
+    return v;
+  }();
   return v;
 }
 static int csr_long_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
+    int v = -1;
     const char *e = getenv("MG_CSR_LONG");
     v = e ? atoi(e) : 0;
-  }
+    return v;
+  }();
   return v;
 }
 
@@ -1046,11 +1057,12 @@ static void launch_csr(const Csr &a, XG x, Epi epi) {
 }
 
 static bool bsell_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static const int on = [] {
+    int on = -1;
     const char *e = getenv("MG_BSELL");
     on = !(e && *e == '0');
-  }
+    return on;
+  }();
   return on;
 }
 
