@@ -155,40 +155,47 @@ __global__ void k_aug_extract(const double *aug, double *inv, int n) {
 // the small MGR F blocks are diagonally dominant in practice).
 constexpr int BGJ = 32;
 
-// the diagonal block D = M_KK inverted in place by one CTA of 32 x 32 threads, one
-// element each, in shared memory: step k reads its pivot row / column entries, syncs,
-// writes (the same arithmetic as a column-per-lane register form: rks = D[k][c] / p,
-// D[i][c] -= D[i][k] * rks), 2 barriers per step instead of 32 dependent shuffles
-__global__ void __launch_bounds__(BGJ * BGJ) k_bgj_diag(double *m, int n, int k0, double *dinv, int *bad) {
-  __shared__ double a[BGJ][BGJ + 1];
+// the diagonal block D = M_KK inverted by one CTA of 32 x 32 threads, one element
+// each, held in a register (warp r = row r).  Step k: warp k alone forms 1/p and its
+// scaled row rks = D[k][c] / p and publishes both in shared memory (double-buffered:
+// one barrier per step, 32 divisions per step instead of 1024 on the FP64 pipe); every
+// thread takes its column entry D[r][k] from lane k of its own warp.  The arithmetic
+// per element is unchanged (rks = D[k][c] * (1/p), D[r][c] -= D[r][k] * rks).
+__global__ void __launch_bounds__(BGJ * BGJ) k_bgj_diag(const double *m, int n, int k0, double *dinv, int *bad) {
+  PDL_ENTRY();
+  __shared__ double prow[2][BGJ + 1];
   const int c = threadIdx.x, r = threadIdx.y;
   const int nb = min(BGJ, n - k0);
-  a[r][c] = (r < nb && c < nb) ? m[(int64_t)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
-  __syncthreads();
+  double a = (r < nb && c < nb) ? m[(int64_t)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
 #pragma unroll 1
   for (int k = 0; k < BGJ; ++k) {
-    const double rk = a[k][c];  // D[k][c]
-    const double ci = a[r][k];  // D[r][k]
-    const double p = a[k][k];
+    double *pr = prow[k & 1];
     if (r == k) {  // warp k holds row k: the pivot test against the row's largest entry
-      double amax = fabs(rk);
+      const double p = __shfl_sync(0xffffffffu, a, k);
+      double amax = fabs(a);
       for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
       if (c == 0 && (!(fabs(p) > 1e-10 * amax) || !(fabs(p) > 1e-300))) atomicCAS(bad, -1, k0 + k);
+      const double ip = 1.0 / p;
+      pr[c] = a * ip;
+      if (c == 0) pr[BGJ] = ip;
     }
     __syncthreads();
-    const double ip = 1.0 / p;
-    const double rks = rk * ip;
-    if (c == k) a[r][k] = (r == k) ? ip : -ci * ip;
-    else if (r == k) a[k][c] = rks;
-    else a[r][c] = a[r][c] - ci * rks;
-    __syncthreads();
+    const double rks = pr[c];
+    const double ip = pr[BGJ];
+    const double ci = __shfl_sync(0xffffffffu, a, k);  // D[r][k]
+    if (c == k) a = (r == k) ? ip : -ci * ip;
+    else if (r == k) a = rks;
+    else a = a - ci * rks;
   }
-  dinv[r * BGJ + c] = a[r][c];
+  dinv[r * BGJ + c] = a;
 }
 
-// M_Kj <- D M_Kj for j outside K: one thread per column j (coalesced across j)
-__global__ void __launch_bounds__(256) k_bgj_rowpanel(double *m, int n, int k0, const double *dinv,
-                                                      const int *bad) {
+// M_Kj <- D M_Kj for j outside K: one thread per column j (coalesced across j);
+// 64-thread CTAs so that the panel's FP64 work spreads over n / 64 SMs
+constexpr int BGJ_PT = 64;
+__global__ void __launch_bounds__(BGJ_PT) k_bgj_rowpanel(double *m, int n, int k0, const double *dinv,
+                                                         const int *bad) {
+  PDL_ENTRY();
   if (*bad >= 0) return;
   __shared__ double d[BGJ][BGJ];
   for (int t = threadIdx.x; t < BGJ * BGJ; t += blockDim.x) d[t / BGJ][t % BGJ] = dinv[t];
@@ -210,6 +217,7 @@ __global__ void __launch_bounds__(256) k_bgj_rowpanel(double *m, int n, int k0, 
 
 // M_ij -= M_iK M_Kj for i, j outside K: 64 x 64 output tile per CTA, 4 x 4 per thread
 __global__ void __launch_bounds__(256) k_bgj_update(double *m, int n, int k0, const int *bad) {
+  PDL_ENTRY();
   if (*bad >= 0) return;
   __shared__ double a[64][BGJ + 1];
   __shared__ double b[BGJ][64 + 1];
@@ -250,8 +258,9 @@ __global__ void __launch_bounds__(256) k_bgj_update(double *m, int n, int k0, co
 }
 
 // M_iK <- -M_iK D (i outside K), M_KK <- D: one thread per row
-__global__ void __launch_bounds__(256) k_bgj_colpanel(double *m, int n, int k0, const double *dinv,
-                                                      const int *bad) {
+__global__ void __launch_bounds__(BGJ_PT) k_bgj_colpanel(double *m, int n, int k0, const double *dinv,
+                                                         const int *bad) {
+  PDL_ENTRY();
   if (*bad >= 0) return;
   __shared__ double d[BGJ][BGJ];
   for (int t = threadIdx.x; t < BGJ * BGJ; t += blockDim.x) d[t / BGJ][t % BGJ] = dinv[t];
@@ -283,12 +292,16 @@ static int blocked_gj(const double *a_dev, double *inv_dev, int n) {
   MG_CUDA(cudaMemcpyAsync(inv_dev, a_dev, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, stream()));
   const dim3 tiles((n + 63) / 64, (n + 63) / 64);
   for (int k0 = 0; k0 < n; k0 += BGJ) {
-    k_bgj_diag<<<1, dim3(BGJ, BGJ), 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
-    k_bgj_rowpanel<<<(n + 255) / 256, 256, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
-    k_bgj_update<<<tiles, 256, 0, stream()>>>(inv_dev, n, k0, bad.p);
-    k_bgj_colpanel<<<(n + 255) / 256, 256, 0, stream()>>>(inv_dev, n, k0, dinv.p, bad.p);
+    // programmatic dependent launch: each kernel waits for its predecessor's
+    // completion on the device, its launch latency hidden behind it
+    launch_pdl(k_bgj_diag, dim3(1), dim3(BGJ, BGJ), 0, (const double *)inv_dev, n, k0, dinv.p, bad.p);
+    launch_pdl(k_bgj_rowpanel, dim3((n + BGJ_PT - 1) / BGJ_PT), dim3(BGJ_PT), 0, inv_dev, n, k0,
+               (const double *)dinv.p, (const int *)bad.p);
+    launch_pdl(k_bgj_update, tiles, dim3(256), 0, inv_dev, n, k0, (const int *)bad.p);
+    launch_pdl(k_bgj_colpanel, dim3((n + BGJ_PT - 1) / BGJ_PT), dim3(BGJ_PT), 0, inv_dev, n, k0,
+               (const double *)dinv.p, (const int *)bad.p);
     check_launch("blocked gj");
-    count_launch(4);
+    count_launch(3);
   }
   int hb = -1;
   d2h(&hb, bad.p, sizeof(int));

@@ -273,3 +273,20 @@ def test_sequence_step_parity(gpu, step):
     assert ro.converged and rg.converged
     assert abs(rg.iterations - ro.iterations) <= 1, (rg.iterations, ro.iterations)
     assert relerr(rg.x, ro.x) <= 1e-8
+
+
+@pytest.mark.parametrize("kind", ["injective", "injection"])
+@pytest.mark.parametrize("cfg,edge", [(1, 32), (2, 20), (3, 24)])
+def test_synthetic_other_rp_kinds_parity(gpu, cfg, edge, kind):
+    """the b = 2 configs run NONINJECTIVE (the north star's literal R / P)
+    by default; the reference schema's other kinds (RpKind, mgr.py:47-51) on the same
+    systems, end to end against the oracle at rtol 1e-10: iterations +-1, solution
+    <= 1e-8."""
+    s = synth.make_config(cfg, edge)
+    rg, _ = gpipe.SyntheticSolver(rel_tol=1e-10, rp=gmgr.RpKind(kind)).solve_system(s)
+    plan_o = opipe.default_plan(s.b, s.n_cells, rp=omgr.RpKind(kind),
+                                frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
+    ro, _, _ = opipe.solve_synthetic(s, rel_tol=1e-10, plan=plan_o, amg_opts=oamg.AmgOptions(**gpipe.DEFAULT_AMG))
+    assert ro.converged and rg.converged
+    assert abs(rg.iterations - ro.iterations) <= 1, (rg.iterations, ro.iterations)
+    assert relerr(rg.x, ro.x) <= 1e-8

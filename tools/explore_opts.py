@@ -4,7 +4,8 @@ and hierarchy shapes for variants of the AMG options and the MGR plan.
     python tools/explore_opts.py CFG EDGE 'label:key=val,key=val' ...
 keys: any AmgOptions field (e.g. coarse_size_cutoff=2000), gr=1 (global block
 relaxation on every MGR level), frpre / frpost (F-relaxation AMG sweeps),
-fr=jacobi|gauss_seidel|amg and frsweeps=N (the F-relaxation kind, mgr.py:159-209).
+fr=jacobi|gauss_seidel|amg and frsweeps=N (the F-relaxation kind, mgr.py:159-209),
+rp=injective|noninjective|injection (RpKind of every MGR level, mgr.py:47-51).
 """
 import os
 import statistics
@@ -14,7 +15,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_1801_08464_b200 import _lib, pipeline, synth  # noqa: E402
-from paper_1801_08464_b200.mgr import FRelax  # noqa: E402
+from paper_1801_08464_b200.mgr import FRelax, RpKind  # noqa: E402
 
 
 def run(ctx, s, label, kv, reps=3, warm=2):
@@ -22,11 +23,14 @@ def run(ctx, s, label, kv, reps=3, warm=2):
     fr_kw = dict(pipeline.DEFAULT_FRELAX)
     gr = False
     fr_kind, fr_sweeps = "amg", 1
+    rp = None
     for k, v in kv.items():
         if k == "gr":
             gr = bool(int(v))
         elif k == "fr":
             fr_kind = v
+        elif k == "rp":
+            rp = RpKind[v.upper()]
         elif k == "frsweeps":
             fr_sweeps = int(v)
         elif k in ("frpre", "frpost"):
@@ -35,7 +39,7 @@ def run(ctx, s, label, kv, reps=3, warm=2):
             amg_kw[k] = type(pipeline.DEFAULT_AMG.get(k, 0))(v) if k in pipeline.DEFAULT_AMG else int(v)
     solver = pipeline.SyntheticSolver(rel_tol=1e-8, ctx=ctx, amg_opts=pipeline.default_amg_options(**amg_kw),
                                       frelax=FRelax("amg", **fr_kw) if fr_kind == "amg" else FRelax(fr_kind, sweeps=fr_sweeps),
-                                      global_relax=gr)
+                                      global_relax=gr, rp=rp)
     solver.upload(s)
     rows = []
     for r in range(warm + reps):
