@@ -143,24 +143,29 @@ __global__ void k_aug_extract(const double *aug, double *inv, int n) {
   }
 }
 
-// ---- blocked in-place Gauss-Jordan without pivoting (n > 256) --------------------
-// Block pivot K = [k0, k0 + 32):  D = M_KK^-1 (one CTA, in shared memory);
-// M_Kj <- D M_Kj (j not in K);  M_ij -= M_iK M_Kj (i, j not in K);
-// M_iK <- -M_iK D (i not in K);  M_KK <- D.  After the last panel M = A^-1.
-// A 32-column rank update per panel instead of one full pass over [A | I] per
-// column: ~2n^3 flops and n/32 x 4 launches (n = 2048: 64 panels) instead of
-// 4n launches.  No pivoting: a pivot that is tiny against its row in the
-// diagonal block (|p| < 1e-10 max|row|) aborts, and dense_inverse falls back to
-// the partially pivoted Gauss-Jordan above (the AMG coarsest operators and
-// the small MGR F blocks are diagonally dominant in practice).
+// ---- blocked Gauss-Jordan without pivoting (n > 256) -----------------------------
+// Block pivot K = [k0, k0 + 32), D = M_KK^-1.  One panel step maps M to M':
+//   M'_Kj = D M_Kj (j not in K);      M'_ij = M_ij - M_iK (D M_Kj) (i, j not in K);
+//   M'_iK = -M_iK D (i not in K);     M'_KK = D.
+// After the last panel M = A^-1.  A panel step is ONE launch, out of place between
+// two n x n buffers (no read / write hazards between CTAs, so no separate row-panel,
+// update and column-panel launches): every CTA forms its own 32 x 64 slice of
+// D M_Kj in shared memory.  The next panel's diagonal block is updated and inverted
+// by one extra CTA of the same launch (look-ahead), so the 32-step dependent chain of
+// the small inverse runs beside the rank-32 update instead of between two launches:
+// n / 32 dependent launches in all (n = 1708: 54 x ~20 us), chained by programmatic
+// dependent launch.  ~3 n^3 FP64 multiply-adds, explicit fma (the inverse is compared
+// with the oracle's LU solve to 1e-12, not bit for bit).  No pivoting: a pivot that is
+// tiny against its row in the diagonal block (|p| < 1e-10 max|row|) aborts, and
+// dense_inverse falls back to the partially pivoted Gauss-Jordan above (the AMG
+// coarsest operators and the small MGR F blocks are diagonally dominant in practice).
 constexpr int BGJ = 32;
 
-// the diagonal block D = M_KK inverted by one CTA of 32 x 32 threads, one element
+// the first diagonal block D = M_KK inverted by one CTA of 32 x 32 threads, one element
 // each, held in a register (warp r = row r).  Step k: warp k alone forms 1/p and its
 // scaled row rks = D[k][c] / p and publishes both in shared memory (double-buffered:
 // one barrier per step, 32 divisions per step instead of 1024 on the FP64 pipe); every
-// thread takes its column entry D[r][k] from lane k of its own warp.  The arithmetic
-// per element is unchanged (rks = D[k][c] * (1/p), D[r][c] -= D[r][k] * rks).
+// thread takes its column entry D[r][k] from lane k of its own warp.
 __global__ void __launch_bounds__(BGJ * BGJ) k_bgj_diag(const double *m, int n, int k0, double *dinv, int *bad) {
   PDL_ENTRY();
   __shared__ double prow[2][BGJ + 1];
@@ -172,9 +177,9 @@ __global__ void __launch_bounds__(BGJ * BGJ) k_bgj_diag(const double *m, int n, 
     double *pr = prow[k & 1];
     if (r == k) {  // warp k holds row k: the pivot test against the row's largest entry
       const double p = __shfl_sync(0xffffffffu, a, k);
-      double amax = fabs(a);
-      for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      if (c == 0 && (!(fabs(p) > 1e-10 * amax) || !(fabs(p) > 1e-300))) atomicCAS(bad, -1, k0 + k);
+      // |p| > 1e-10 max_c |a_c|  <=>  |p| > 1e-10 |a_c| on every lane: one vote
+      const bool ok = __all_sync(0xffffffffu, fabs(p) > 1e-10 * fabs(a)) && fabs(p) > 1e-300;
+      if (c == 0 && !ok) atomicCAS(bad, -1, k0 + k);
       const double ip = 1.0 / p;
       pr[c] = a * ip;
       if (c == 0) pr[BGJ] = ip;
@@ -190,118 +195,171 @@ __global__ void __launch_bounds__(BGJ * BGJ) k_bgj_diag(const double *m, int n, 
   dinv[r * BGJ + c] = a;
 }
 
-// M_Kj <- D M_Kj for j outside K: one thread per column j (coalesced across j);
-// 64-thread CTAs so that the panel's FP64 work spreads over n / 64 SMs
-constexpr int BGJ_PT = 64;
-__global__ void __launch_bounds__(BGJ_PT) k_bgj_rowpanel(double *m, int n, int k0, const double *dinv,
-                                                         const int *bad) {
+// One panel step src -> dst (see above).  Block 0: look-ahead (the next diagonal
+// block of dst, inverted into dnext); blocks 1..: 64 x 64 output tiles, 4 x 4 per
+// thread.  256 threads.
+__global__ void __launch_bounds__(256, 3) k_bgj_panel(const double *__restrict__ src, double *__restrict__ dst, int n,
+                                                   int k0, const double *__restrict__ dcur, double *dnext,
+                                                   int tiles_x, int *bad) {
   PDL_ENTRY();
-  if (*bad >= 0) return;
-  __shared__ double d[BGJ][BGJ];
-  for (int t = threadIdx.x; t < BGJ * BGJ; t += blockDim.x) d[t / BGJ][t % BGJ] = dinv[t];
+  // the flag can be raised by this launch's own look-ahead CTA: one read per CTA,
+  // so that a CTA leaves as a whole
+  __shared__ int sbad;
+  if (threadIdx.x == 0) sbad = *(volatile int *)bad;
   __syncthreads();
+  if (sbad >= 0) return;
+  __shared__ double sa[64][BGJ + 1];   // M_iK
+  __shared__ double sb[BGJ][64 + 1];   // M_Kj, then D M_Kj (columns of K: D)
+  __shared__ double sd[BGJ][BGJ + 1];  // D
+  const int tid = threadIdx.x;
   const int nb = min(BGJ, n - k0);
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n || (j >= k0 && j < k0 + nb)) return;
-  double x[BGJ];
+  for (int t = tid; t < BGJ * BGJ; t += 256) sd[t / BGJ][t % BGJ] = dcur[t];
+  if (blockIdx.x == 0) {
+    // ---- look-ahead: U = M_R'R' - M_R'K (D M_KR'), R' = [k0 + 32, k0 + 32 + nbn), then U^-1
+    const int r0 = k0 + BGJ;
+    const int nbn = min(BGJ, n - r0);
+    if (nbn <= 0) return;
+    __shared__ double prow[2][BGJ + 1];
+    for (int t = tid; t < BGJ * BGJ; t += 256) {
+      const int r = t / BGJ, c = t % BGJ;
+      sa[r][c] = (r < nbn && c < nb) ? src[(int64_t)(r0 + r) * n + k0 + c] : 0.0;
+      sb[r][c] = (r < nb && c < nbn) ? src[(int64_t)(k0 + r) * n + r0 + c] : 0.0;
+    }
+    __syncthreads();
+    const int w = tid >> 5, c = tid & 31;  // thread (w, c) holds rows q * 8 + w, column c
+    double t4[4];
 #pragma unroll
-  for (int k = 0; k < BGJ; ++k) x[k] = k < nb ? m[(int64_t)(k0 + k) * n + j] : 0.0;
-#pragma unroll 4
-  for (int r = 0; r < nb; ++r) {
-    double s = 0.0;
+    for (int q = 0; q < 4; ++q) {
+      double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < BGJ; ++k) s += d[r][k] * x[k];
-    m[(int64_t)(k0 + r) * n + j] = s;
+      for (int k = 0; k < BGJ; ++k) s = fma(sd[q * 8 + w][k], sb[k][c], s);
+      t4[q] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sb[q * 8 + w][c] = t4[q];
+    __syncthreads();
+    double a[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = q * 8 + w;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < BGJ; ++k) s = fma(sa[r][k], sb[k][c], s);
+      a[q] = (r < nbn && c < nbn) ? src[(int64_t)(r0 + r) * n + r0 + c] - s : (r == c ? 1.0 : 0.0);
+    }
+    // register-resident Gauss-Jordan (as k_bgj_diag, four rows per thread); fully
+    // unrolled so that the owner slot k / 8 is a compile-time register index
+#pragma unroll
+    for (int k = 0; k < BGJ; ++k) {
+      double *pr = prow[k & 1];
+      if (w == (k & 7)) {
+        const double ak = a[k >> 3];
+        const double p = __shfl_sync(0xffffffffu, ak, k);
+        const bool ok = __all_sync(0xffffffffu, fabs(p) > 1e-10 * fabs(ak)) && fabs(p) > 1e-300;
+        if (c == 0 && !ok) atomicCAS(bad, -1, r0 + k);
+        const double ip = 1.0 / p;
+        pr[c] = ak * ip;
+        if (c == 0) pr[BGJ] = ip;
+      }
+      __syncthreads();
+      const double rks = pr[c];
+      const double ip = pr[BGJ];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = q * 8 + w;
+        const double ci = __shfl_sync(0xffffffffu, a[q], k);
+        if (c == k) a[q] = (r == k) ? ip : -ci * ip;
+        else if (r == k) a[q] = rks;
+        else a[q] = a[q] - ci * rks;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dnext[(q * 8 + w) * BGJ + c] = a[q];
+    return;
   }
-}
-
-// M_ij -= M_iK M_Kj for i, j outside K: 64 x 64 output tile per CTA, 4 x 4 per thread
-__global__ void __launch_bounds__(256) k_bgj_update(double *m, int n, int k0, const int *bad) {
-  PDL_ENTRY();
-  if (*bad >= 0) return;
-  __shared__ double a[64][BGJ + 1];
-  __shared__ double b[BGJ][64 + 1];
-  const int nb = min(BGJ, n - k0);
-  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-  for (int t = threadIdx.x; t < 64 * BGJ; t += 256) {
+  // ---- a 64 x 64 tile of dst
+  const int tile = blockIdx.x - 1;
+  const int i0 = (tile / tiles_x) * 64, j0 = (tile % tiles_x) * 64;
+  for (int t = tid; t < 64 * BGJ; t += 256) {
     const int ii = t / BGJ, kk = t % BGJ;
     const int i = i0 + ii;
-    a[ii][kk] = (i < n && kk < nb) ? m[(int64_t)i * n + k0 + kk] : 0.0;
+    sa[ii][kk] = (i < n && kk < nb) ? src[(int64_t)i * n + k0 + kk] : 0.0;
     const int kb = t / 64, jj = t % 64;
     const int j = j0 + jj;
-    b[kb][jj] = (j < n && kb < nb) ? m[(int64_t)(k0 + kb) * n + j] : 0.0;
+    sb[kb][jj] = (j < n && kb < nb) ? src[(int64_t)(k0 + kb) * n + j] : 0.0;
   }
   __syncthreads();
-  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+  {
+    // column jj of sb <- D * (column jj), columns of K <- D: 4 threads per column, 8 rows each
+    const int jj = tid & 63, rg = tid >> 6;
+    const int j = j0 + jj;
+    const bool in_k = j >= k0 && j < k0 + nb;
+    double out[8] = {};
+#pragma unroll 8
+    for (int k = 0; k < BGJ; ++k) {
+      const double ck = sb[k][jj];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) out[q] = fma(sd[rg * 8 + q][k], ck, out[q]);
+    }
+    if (in_k) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) out[q] = sd[rg * 8 + q][j - k0];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sb[rg * 8 + q][jj] = out[q];
+  }
+  __syncthreads();
+  const int tr = tid / 16, tc = tid % 16;
   double acc[4][4] = {};
 #pragma unroll 8
   for (int k = 0; k < BGJ; ++k) {
     double av[4], bv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { av[u] = a[tr + 16 * u][k]; bv[u] = b[k][tc + 16 * u]; }
+    for (int u = 0; u < 4; ++u) { av[u] = sa[tr + 16 * u][k]; bv[u] = sb[k][tc + 16 * u]; }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] += av[u] * bv[v];
+      for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int i = i0 + tr + 16 * u;
-    if (i >= n || (i >= k0 && i < k0 + nb)) continue;
+    if (i >= n) continue;
+    const bool i_in_k = i >= k0 && i < k0 + nb;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int j = j0 + tc + 16 * v;
-      if (j >= n || (j >= k0 && j < k0 + nb)) continue;
-      m[(int64_t)i * n + j] -= acc[u][v];
+      const int jj = tc + 16 * v, j = j0 + jj;
+      if (j >= n) continue;
+      const bool j_in_k = j >= k0 && j < k0 + nb;
+      double o;
+      if (i_in_k) o = sb[i - k0][jj];
+      else o = (j_in_k ? 0.0 : src[(int64_t)i * n + j]) - acc[u][v];
+      dst[(int64_t)i * n + j] = o;
     }
-  }
-}
-
-// M_iK <- -M_iK D (i outside K), M_KK <- D: one thread per row
-__global__ void __launch_bounds__(BGJ_PT) k_bgj_colpanel(double *m, int n, int k0, const double *dinv,
-                                                         const int *bad) {
-  PDL_ENTRY();
-  if (*bad >= 0) return;
-  __shared__ double d[BGJ][BGJ];
-  for (int t = threadIdx.x; t < BGJ * BGJ; t += blockDim.x) d[t / BGJ][t % BGJ] = dinv[t];
-  __syncthreads();
-  const int nb = min(BGJ, n - k0);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double *row = m + (int64_t)i * n + k0;
-  if (i >= k0 && i < k0 + nb) {
-    for (int c = 0; c < nb; ++c) row[c] = d[i - k0][c];
-    return;
-  }
-  double x[BGJ];
-#pragma unroll
-  for (int k = 0; k < BGJ; ++k) x[k] = k < nb ? row[k] : 0.0;
-  for (int c = 0; c < nb; ++c) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < BGJ; ++k) s += x[k] * d[k][c];
-    row[c] = -s;
   }
 }
 
 // n > 256: returns -1 on success, else the global index of a rejected pivot
 static int blocked_gj(const double *a_dev, double *inv_dev, int n) {
-  DBuf<double> dinv(BGJ * BGJ);
+  DBuf<double> dinv(2 * BGJ * BGJ), tmp((size_t)n * n);
   DBuf<int> bad(1);
   dset_i32(bad.p, {-1});
-  MG_CUDA(cudaMemcpyAsync(inv_dev, a_dev, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, stream()));
-  const dim3 tiles((n + 63) / 64, (n + 63) / 64);
-  for (int k0 = 0; k0 < n; k0 += BGJ) {
-    // programmatic dependent launch: each kernel waits for its predecessor's
+  const int npan = (n + BGJ - 1) / BGJ;
+  // panel p reads buf[p & 1] and writes buf[(p + 1) & 1]: the last one lands in inv_dev
+  double *buf[2] = {(npan & 1) ? tmp.p : inv_dev, (npan & 1) ? inv_dev : tmp.p};
+  MG_CUDA(cudaMemcpyAsync(buf[0], a_dev, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, stream()));
+  launch_pdl(k_bgj_diag, dim3(1), dim3(BGJ, BGJ), 0, (const double *)buf[0], n, 0, dinv.p, bad.p);
+  check_launch("blocked gj diag");
+  const int tx = (n + 63) / 64;
+  for (int p = 0; p < npan; ++p) {
+    // programmatic dependent launch: each panel waits for its predecessor's
     // completion on the device, its launch latency hidden behind it
-    launch_pdl(k_bgj_diag, dim3(1), dim3(BGJ, BGJ), 0, (const double *)inv_dev, n, k0, dinv.p, bad.p);
-    launch_pdl(k_bgj_rowpanel, dim3((n + BGJ_PT - 1) / BGJ_PT), dim3(BGJ_PT), 0, inv_dev, n, k0,
-               (const double *)dinv.p, (const int *)bad.p);
-    launch_pdl(k_bgj_update, tiles, dim3(256), 0, inv_dev, n, k0, (const int *)bad.p);
-    launch_pdl(k_bgj_colpanel, dim3((n + BGJ_PT - 1) / BGJ_PT), dim3(BGJ_PT), 0, inv_dev, n, k0,
-               (const double *)dinv.p, (const int *)bad.p);
-    check_launch("blocked gj");
-    count_launch(3);
+    launch_pdl(k_bgj_panel, dim3(1 + tx * tx), dim3(256), 0, (const double *)buf[p & 1], buf[(p + 1) & 1], n,
+               p * BGJ, (const double *)(dinv.p + (p & 1) * BGJ * BGJ), dinv.p + ((p + 1) & 1) * BGJ * BGJ, tx,
+               bad.p);
+    check_launch("blocked gj panel");
   }
   int hb = -1;
   d2h(&hb, bad.p, sizeof(int));

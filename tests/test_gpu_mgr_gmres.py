@@ -290,3 +290,23 @@ def test_synthetic_other_rp_kinds_parity(gpu, cfg, edge, kind):
     assert ro.converged and rg.converged
     assert abs(rg.iterations - ro.iterations) <= 1, (rg.iterations, ro.iterations)
     assert relerr(rg.x, ro.x) <= 1e-8
+
+
+@pytest.mark.parametrize("nf", [257, 320, 1001, 1708])
+def test_blocked_dense_inverse_sizes(gpu, nf):
+    """The blocked Gauss-Jordan inverse behind FRelax('exact') / coarse='exact' / the AMG
+    coarsest level (amg.py:330-343), at sizes with a partial last panel, an odd and an even
+    panel count: the MGR apply through it matches the oracle's LU solves within 1e-12."""
+    rng = np.random.default_rng(nf)
+    nc = 40
+    n = nf + nc
+    a = sp.random(n, n, density=min(1.0, 12.0 / n), random_state=rng, format="csr") * 0.2
+    a = a + sp.diags(rng.uniform(3.0, 5.0, n))
+    A = sp.csr_matrix(a)
+    f = np.arange(nf)
+    so, sg = spec_pair("injective", "exact")
+    ho = omgr.setup_from_matrix(A, [(f, so)], coarse="exact")
+    hg = gmgr.setup_from_matrix(A, [(f, sg)], coarse="exact")
+    for _ in range(2):
+        r = rng.standard_normal(n)
+        assert relerr(gmgr.mgr_apply(hg, r), omgr.mgr_apply(ho, r)) <= 1e-12
