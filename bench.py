@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--edge", type=int, default=None)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-variants", action="store_true",
+                   help="skip the R/P-kind side measurements (SURVEY D5) after the timed run")
     return p.parse_args()
 
 
@@ -434,6 +436,11 @@ def main():
     if not args.no_e2e:
         e2e = _e2e(ctx, sysm, args, rep, barrier)
 
+    # ---- side measurement (not the headline): the reference schema's other R/P kinds ----
+    variants = None
+    if rank == 0 and ws == 1 and sysm.b == 2 and not args.no_variants:
+        variants = _rp_variants(ctx, sysm, b_dev, x_dev, n)
+
     cpu = cpu_job.result() if cpu_job is not None else None
 
     if rank == 0:
@@ -450,8 +457,50 @@ def main():
                 "roofline_spmv": spmv_roof,
                 "solve_phase_ms": phases,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+        if variants:
+            line["rp_kinds"] = variants
         print(json.dumps(line), flush=True)
     rep.close()
+
+
+def _rp_variants(ctx, sysm, b_dev, x_dev, n, warm=2, reps=3):
+    """SURVEY D5 asks for both R/P kinds on the b = 2 configs.  The headline runs
+    RpKind.NONINJECTIVE (the north star's literal R = [-A_cf A_ff^-1, I], P = [-A_ff^-1 A_fc; I]
+    with the diagonal of A_ff); this times the same setup + solve step on the same resident
+    system with the schema's INJECTIVE (R = [0, I]) and INJECTION (R = [0, I], P = [0; I]) kinds
+    (mgr.py:47-51), after the timed region, device events on the library stream."""
+    from paper_1801_08464_b200 import _lib
+    from paper_1801_08464_b200.mgr import RpKind
+    from paper_1801_08464_b200.pipeline import SyntheticSolver
+    out = {"note": "side measurement after the timed region; the headline value is the noninjective kind"}
+    for kind in (RpKind.INJECTIVE, RpKind.INJECTION):
+        sv = SyntheticSolver(rel_tol=1e-8, restart=30, max_iter=400, ctx=ctx, rp=kind)
+        a = sv.upload(sysm)
+        gopts = sv.gopts.to_c()
+        res = _lib.GmresRes()
+        ev = _Events(ctx)
+        sm, so = [], []
+        for r in range(warm + reps):
+            if r == warm:
+                ctx.sync()
+                ev.record_start()
+            sv.setup()
+            ctx.call("mg_gmres_dev", a.h, sv.hier.h, b_dev, x_dev, _lib.ctypes.byref(gopts), -1.0,
+                     _lib.ctypes.byref(res))
+            if r >= warm:
+                t = ctx.timing()
+                sm.append(t.setup_ms)
+                so.append(t.solve_ms)
+        ev.record_stop()
+        ctx.sync()
+        ms = ev.elapsed_ms() / reps
+        out[kind.value] = {"value": n / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "iterations": int(res.iterations),
+                           "converged": bool(res.converged), "setup_ms": statistics.median(sm),
+                           "solve_ms": statistics.median(so)}
+        sv.hier.free()
+        sv.hier = None
+        a.free()
+    return out
 
 
 class _Events:
