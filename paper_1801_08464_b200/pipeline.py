@@ -82,9 +82,13 @@ class SyntheticSolver:
         self.ahat = None
         self._plan = None
 
-    def upload(self, sysm) -> DeviceMatrix:
+    def upload(self, sysm, asynchronous=False) -> DeviceMatrix:
+        """Upload the system's block CSR matrix.  ``asynchronous=True`` copies on the
+        context's copy stream (mg_mat_upload_bsr_async) and returns at once: the arrays
+        should be pinned (see PinnedSystem) so that the copy overlaps the solve of the
+        previous system of a sequence."""
         self.sysm_meta = (sysm.b, sysm.n_cells)
-        self.a = DeviceMatrix.from_bsr(sysm.rowptr, sysm.col, sysm.vals, ctx=self.ctx)
+        self.a = DeviceMatrix.from_bsr(sysm.rowptr, sysm.col, sysm.vals, ctx=self.ctx, asynchronous=asynchronous)
         return self.a
 
     def setup(self, a: DeviceMatrix | None = None, b: int | None = None, n_cells: int | None = None):
@@ -126,3 +130,37 @@ class SyntheticSolver:
                         converged=res.converged,
                         relres=res.residual_norm / res.rhs_norm if res.rhs_norm else 0.0)
         return res, st
+
+
+class PinnedSystem:
+    """Page-locked host staging for one synthetic system of a sequence (BASELINE config 5:
+    20 successive 128^3 systems): the producer writes the next system here while the GPU
+    solves the current one, and upload(asynchronous=True) copies it on the copy stream.
+    Same fields as synth.BlockSystem as far as SyntheticSolver reads them."""
+
+    def __init__(self, like):
+        import torch
+        self._keep = []
+
+        def pin(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            self._keep.append(t)
+            return t.numpy()
+
+        self.rowptr, self.col, self.vals, self.rhs = pin(like.rowptr), pin(like.col), pin(like.vals), pin(like.rhs)
+        self._meta(like)
+
+    def _meta(self, s):
+        self.b, self.n_cells, self.n, self.nnzb = s.b, s.n_cells, s.n, s.nnzb
+
+    def load(self, s):
+        """Copy another system of the same block pattern size into the pinned arrays."""
+        if s.rowptr.shape != self.rowptr.shape or s.col.shape != self.col.shape or s.vals.shape != self.vals.shape:
+            raise ValueError("PinnedSystem.load: the system's shape differs from the staging buffers'")
+        np.copyto(self.rowptr, s.rowptr)
+        np.copyto(self.col, s.col)
+        np.copyto(self.vals, s.vals)
+        np.copyto(self.rhs, s.rhs)
+        self._meta(s)
+        return self
+

@@ -310,3 +310,32 @@ def test_blocked_dense_inverse_sizes(gpu, nf):
     for _ in range(2):
         r = rng.standard_normal(n)
         assert relerr(gmgr.mgr_apply(hg, r), omgr.mgr_apply(ho, r)) <= 1e-12
+
+
+def test_sequence_pipelined_upload_matches_synchronous(gpu):
+    """BASELINE config 5's sequence as a pipeline: the next system staged in pinned memory
+    and copied on the copy stream (mg_mat_upload_bsr_async) while the current one is set up
+    and solved, one solver reused -- every step's solution and iteration count equal the
+    synchronous solve_system of the same step bit for bit."""
+    nsteps = 4
+    systems = [synth.make_config(5, 20, step=k) for k in range(nsteps)]
+    ref = []
+    for s in systems:
+        r, _ = gpipe.SyntheticSolver(rel_tol=1e-10).solve_system(s)
+        ref.append(r)
+    stage = [gpipe.PinnedSystem(systems[0]), gpipe.PinnedSystem(systems[1])]
+    sol = gpipe.SyntheticSolver(rel_tol=1e-10)
+    nxt = sol.upload(stage[0], asynchronous=True)
+    for k in range(nsteps):
+        cur = stage[k & 1]
+        a = nxt
+        nxt = sol.upload(stage[(k + 1) & 1], asynchronous=True) if k + 1 < nsteps else None
+        sol.a = a
+        sol.sysm_meta = (cur.b, cur.n_cells)
+        sol.setup(a)
+        r = sol.solve(cur.rhs)
+        a.free()
+        if k + 2 < nsteps:
+            stage[k & 1].load(systems[k + 2])
+        assert r.iterations == ref[k].iterations
+        np.testing.assert_array_equal(r.x.view(np.int64), ref[k].x.view(np.int64))
