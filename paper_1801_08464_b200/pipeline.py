@@ -68,7 +68,7 @@ class SyntheticSolver:
     """Upload once, then setup / solve on the device."""
 
     def __init__(self, rel_tol=1e-8, restart=30, max_iter=400, amg_opts=None, rp=None, frelax=None, ctx=None,
-                 orthogonalization="dcgs2", global_relax=False):
+                 orthogonalization="dcgs2", global_relax=False, post_smoothing=False):
         self.ctx = ctx or _lib.ctx()
         self.gopts = GmresOptions(rel_tol=rel_tol, restart=restart, max_iter=max_iter,
                                   orthogonalization=orthogonalization)
@@ -76,6 +76,7 @@ class SyntheticSolver:
         self.rp = rp
         self.frelax = frelax
         self.global_relax = global_relax  # per-cell block relaxation on every MGR level (mgr.py:212-251)
+        self.post_smoothing = post_smoothing  # F-relaxation again after the coarse correction (mgr.py:372-376)
         self.a: DeviceMatrix | None = None
         self.hier: MgrHierarchy | None = None
         self.dinv = None
@@ -108,7 +109,8 @@ class SyntheticSolver:
             self._plan = (key, compile_plan(default_plan(b, n_cells, self.rp, self.frelax, self.global_relax),
                                             a.nrows))
         cells = np.repeat(np.arange(n_cells, dtype=np.int64), b) if self.global_relax else None
-        self.hier = setup_from_matrix(self.ahat, self._plan[1], self.amg_opts, cells=cells)
+        self.hier = setup_from_matrix(self.ahat, self._plan[1], self.amg_opts, cells=cells,
+                                      post_smoothing=self.post_smoothing)
         self.hier.set_prescale(self.dinv)
         # Ahat is copied into the hierarchy; release the standalone copy
         self.ahat.free()

@@ -5,7 +5,8 @@ and hierarchy shapes for variants of the AMG options and the MGR plan.
 keys: any AmgOptions field (e.g. coarse_size_cutoff=2000), gr=1 (global block
 relaxation on every MGR level), frpre / frpost (F-relaxation AMG sweeps),
 fr=jacobi|gauss_seidel|amg and frsweeps=N (the F-relaxation kind, mgr.py:159-209),
-rp=injective|noninjective|injection (RpKind of every MGR level, mgr.py:47-51).
+rp=injective|noninjective|injection (RpKind of every MGR level, mgr.py:47-51),
+post=1 (MGR post-smoothing: the F-relaxation again after the coarse correction), frmax=N (FRelax.max_levels).
 """
 import os
 import statistics
@@ -24,6 +25,7 @@ def run(ctx, s, label, kv, reps=3, warm=2):
     gr = False
     fr_kind, fr_sweeps = "amg", 1
     rp = None
+    post = False
     for k, v in kv.items():
         if k == "gr":
             gr = bool(int(v))
@@ -31,6 +33,10 @@ def run(ctx, s, label, kv, reps=3, warm=2):
             fr_kind = v
         elif k == "rp":
             rp = RpKind[v.upper()]
+        elif k == "post":
+            post = bool(int(v))
+        elif k == "frmax":
+            fr_kw["max_levels"] = int(v)
         elif k == "frsweeps":
             fr_sweeps = int(v)
         elif k in ("frpre", "frpost"):
@@ -39,7 +45,7 @@ def run(ctx, s, label, kv, reps=3, warm=2):
             amg_kw[k] = type(pipeline.DEFAULT_AMG.get(k, 0))(v) if k in pipeline.DEFAULT_AMG else int(v)
     solver = pipeline.SyntheticSolver(rel_tol=1e-8, ctx=ctx, amg_opts=pipeline.default_amg_options(**amg_kw),
                                       frelax=FRelax("amg", **fr_kw) if fr_kind == "amg" else FRelax(fr_kind, sweeps=fr_sweeps),
-                                      global_relax=gr, rp=rp)
+                                      global_relax=gr, rp=rp, post_smoothing=post)
     solver.upload(s)
     rows = []
     for r in range(warm + reps):
