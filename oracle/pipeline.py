@@ -35,15 +35,25 @@ def scalar_a(sysm):
     return synth.to_scalar_csr(sysm, order="cell", drop_zeros=False)
 
 
-def setup_synthetic(sysm, *, amg_opts=None, rp=None, plan=None):
+def default_post_smoothing(b):
+    """MGR sweep order (mgr.py:362-368) of the synthetic pipeline: for the b = 2 configs the
+    coarse correction first and the F-relaxation after it (``post_smoothing=True``), for
+    b = 3 the reference default (F-relaxation first).  Mirrors
+    paper_1801_08464_b200.pipeline.default_post_smoothing."""
+    return b == 2
+
+
+def setup_synthetic(sysm, *, amg_opts=None, rp=None, plan=None, post_smoothing=None):
     """A (scalar CSR, cell-major), the per-cell prescale and the MGR hierarchy on Â."""
     t0 = time.perf_counter()
     a = scalar_a(sysm)
     dinv, ahat = blockscale.block_scale(sysm)
     if plan is None:
         plan = default_plan(sysm.b, sysm.n_cells, rp)
+    if post_smoothing is None:
+        post_smoothing = default_post_smoothing(sysm.b)
     opts = amg_opts or oamg.AmgOptions(coarse_size_cutoff=2000)
-    hier = mgr.setup_from_matrix(CsrMatrix(ahat), plan, opts)
+    hier = mgr.setup_from_matrix(CsrMatrix(ahat), plan, opts, post_smoothing=post_smoothing)
     return (a, dinv, hier), time.perf_counter() - t0
 
 
@@ -95,8 +105,8 @@ def _noisy(y, eps, rng):
 
 
 def solve_synthetic(sysm, *, rel_tol=1e-8, restart=30, max_iter=400, amg_opts=None,
-                    rp=None, plan=None, perturb_seed=None):
-    state, setup_s = setup_synthetic(sysm, amg_opts=amg_opts, rp=rp, plan=plan)
+                    rp=None, plan=None, perturb_seed=None, post_smoothing=None):
+    state, setup_s = setup_synthetic(sysm, amg_opts=amg_opts, rp=rp, plan=plan, post_smoothing=post_smoothing)
     t1 = time.perf_counter()
     res = gmres_synthetic(state, sysm.rhs, rel_tol=rel_tol, restart=restart, max_iter=max_iter,
                           perturb_seed=perturb_seed)

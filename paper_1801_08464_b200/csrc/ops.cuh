@@ -33,6 +33,10 @@ void vsub(double *r, const double *b, const double *ax, int64_t n);         // r
 void gather(double *dst, const double *src, const int *idx, int64_t n);     // dst[i] = src[idx[i]]
 void scatter_add(double *dst, const double *src, const int *idx, int64_t n);// dst[idx[i]] += src[i]
 // dst = src[idx]; bs = sign .* dst (when sign); xo = d .* (bs or dst)
+// y = b[rows] - A x for a row-extracted operator A (rows = the source rows), plus the
+// EpiStoreScale outputs when xo is given (xo = d .* (sign .* y))
+void residual_rows_scale(const Csr &a, const double *x, const double *b, const int *rows, double *y,
+                         const double *sign, double *bs, const double *d, double *xo);
 void gather_scale(double *dst, const double *src, const int *idx, int64_t n, const double *sign, double *bs,
                   const double *d, double *xo);
 void scatter_set(double *dst, const double *src, const int *idx, int64_t n);// dst[idx[i]] = src[i]

@@ -631,7 +631,16 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
       {
         MgrLevel *lvp = &lv;
         const bool want_af = !post_smoothing && !sp.global_relax;
-        tasks.run([lvp, want_af, n]() {
+        const bool want_afr = post_smoothing && !sp.global_relax;
+        tasks.run([lvp, want_af, want_afr, n]() {
+          if (want_afr) {
+            // coarse correction first: the F-relaxation that follows needs the residual
+            // r - A e on the F rows only (half of A), written densely in F order
+            DBuf<int> allcols(n);
+            iota_i32(allcols.p, n);
+            lvp->AFr = extract(lvp->A, lvp->flist.p, lvp->nf, allcols.p, n);
+            prepare_spmv(lvp->AFr);
+          }
           if (want_af) {
             // after the F-relaxation from e = 0, e is zero on C: r - A e = r - A[:, F] e_F
             DBuf<int> allrows(n);
@@ -639,7 +648,7 @@ std::unique_ptr<Mgr> mgr_setup(const Csr &a, const std::vector<LevelSpec> &plan,
             lvp->AF = extract(lvp->A, allrows.p, n, lvp->fmap.p, lvp->nf);
             prepare_spmv(lvp->AF);
           }
-          prepare_spmv(lvp->A);
+          if (!want_afr) prepare_spmv(lvp->A);  // with A[F, :] the apply never multiplies by A itself
           prepare_spmv(lvp->R);
           prepare_spmv(lvp->P);
           lvp->res.alloc(n);
@@ -709,12 +718,17 @@ static void apply_level(Mgr &h, size_t k, const double *r, double *e, bool pre_d
     bool pre = false;
     {
       ProfScope ps(4);
-      const double *rr = resid();
       // the F-relaxation AMG's first pre-sweep (x = D^-1 r_F) is formed by the gather
       AmgPreTargets t;
       if (lv.fs.kind == FR_AMG) t = amg_pre_targets(*lv.fs.amg, lv.eF.p);
-      if (t.ok) gather_scale(lv.rF.p, rr, lv.flist.p, lv.nf, t.sign, t.bs, t.d, t.xo);
-      else gather(lv.rF.p, rr, lv.flist.p, lv.nf);
+      if (!zero && lv.AFr.nr) {
+        // r_F = r[F] - A[F, :] e in one pass over half of A (no full residual, no gather)
+        residual_rows_scale(lv.AFr, e, r, lv.flist.p, lv.rF.p, t.sign, t.bs, t.d, t.ok ? t.xo : nullptr);
+      } else {
+        const double *rr = resid();
+        if (t.ok) gather_scale(lv.rF.p, rr, lv.flist.p, lv.nf, t.sign, t.bs, t.d, t.xo);
+        else gather(lv.rF.p, rr, lv.flist.p, lv.nf);
+      }
       pre = t.ok;
     }
     {

@@ -80,6 +80,7 @@ struct BlockDiag {             // per-cell block-diagonal relaxation (mgr.py:212
 struct MgrLevel {
   Csr A, R, P, Aff;
   Csr AF;                      // A[:, F] (F-local columns): residual after F-relaxation from e = 0
+  Csr AFr;                     // A[F, :] (post_smoothing): the F rows of the residual before the F-relaxation
   int n = 0, nf = 0, nc = 0, rp = 0;
   DBuf<int> flist, clist, fmap;
   FSolver fs;

@@ -53,6 +53,29 @@ struct EpiStoreScale {
     xo[r] = d[r] * s;
   }
 };
+// rows F of a residual, r_F = b[rows] - A[F, :] x, stored densely in F order, with the
+// F-relaxation AMG's first pre-sweep from zero folded in as in EpiStoreScale (replaces
+// residual on the whole of A + gather_scale: same differences, same products)
+struct EpiResidRowsScale {
+  const double *b;
+  const int *rows;
+  double *y;
+  const double *sign;
+  double *bs;
+  const double *d;
+  double *xo;
+  __device__ void operator()(int i, double s) const {
+    s = b[rows[i]] - s;
+    y[i] = s;
+    if (xo) {
+      if (sign) {
+        s = sign[i] * s;
+        bs[i] = s;
+      }
+      xo[i] = d[i] * s;
+    }
+  }
+};
 struct EpiJacobi {
   const double *x, *b, *dinv;
   double *xo;
@@ -1115,6 +1138,12 @@ void spmv_store_scale(const Csr &a, const double *x, double *y, const double *si
                       double *xo) {
   if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "spmv_store_scale: scalar CSR only");
   launch_csr(a, XPlain{x}, EpiStoreScale{y, sign, bs, d, xo});
+}
+
+void residual_rows_scale(const Csr &a, const double *x, const double *b, const int *rows, double *y,
+                         const double *sign, double *bs, const double *d, double *xo) {
+  if (a.b != 1) throw MgError(MG_ERR_UNSUPPORTED, "residual_rows_scale: scalar CSR only");
+  launch_csr(a, XPlain{x}, EpiResidRowsScale{b, rows, y, sign, bs, d, xo});
 }
 
 void jacobi_sweep(const Csr &a, const double *x, const double *b, const double *dinv, double *xo) {

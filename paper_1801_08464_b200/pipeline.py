@@ -46,6 +46,14 @@ def default_amg_options(**kw) -> AmgOptions:
     return AmgOptions(**d)
 
 
+def default_post_smoothing(b: int) -> bool:
+    """MGR sweep order of the synthetic pipeline (mgr.py:362-368, ``post_smoothing``): for
+    the b = 2 configs the coarse correction runs first and the F-relaxation after it (fewer
+    GMRES iterations on every b = 2 config and size); b = 3 keeps the
+    reference default (F-relaxation first).  The oracle pipeline mirrors this."""
+    return b == 2
+
+
 def default_plan(b: int, n_cells: int, rp=None, frelax: FRelax | None = None, global_relax=False):
     from .synth import mgr_f_indices
     if rp is None:
@@ -68,7 +76,7 @@ class SyntheticSolver:
     """Upload once, then setup / solve on the device."""
 
     def __init__(self, rel_tol=1e-8, restart=30, max_iter=400, amg_opts=None, rp=None, frelax=None, ctx=None,
-                 orthogonalization="dcgs2", global_relax=False, post_smoothing=False):
+                 orthogonalization="dcgs2", global_relax=False, post_smoothing=None):
         self.ctx = ctx or _lib.ctx()
         self.gopts = GmresOptions(rel_tol=rel_tol, restart=restart, max_iter=max_iter,
                                   orthogonalization=orthogonalization)
@@ -76,7 +84,9 @@ class SyntheticSolver:
         self.rp = rp
         self.frelax = frelax
         self.global_relax = global_relax  # per-cell block relaxation on every MGR level (mgr.py:212-251)
-        self.post_smoothing = post_smoothing  # F-relaxation again after the coarse correction (mgr.py:372-376)
+        # MGR sweep order (mgr.py:362-368): True = coarse correction, then F-relaxation;
+        # None = default_post_smoothing(b)
+        self.post_smoothing = post_smoothing
         self.a: DeviceMatrix | None = None
         self.hier: MgrHierarchy | None = None
         self.dinv = None
@@ -109,8 +119,8 @@ class SyntheticSolver:
             self._plan = (key, compile_plan(default_plan(b, n_cells, self.rp, self.frelax, self.global_relax),
                                             a.nrows))
         cells = np.repeat(np.arange(n_cells, dtype=np.int64), b) if self.global_relax else None
-        self.hier = setup_from_matrix(self.ahat, self._plan[1], self.amg_opts, cells=cells,
-                                      post_smoothing=self.post_smoothing)
+        post = default_post_smoothing(b) if self.post_smoothing is None else self.post_smoothing
+        self.hier = setup_from_matrix(self.ahat, self._plan[1], self.amg_opts, cells=cells, post_smoothing=post)
         self.hier.set_prescale(self.dinv)
         # Ahat is copied into the hierarchy; release the standalone copy
         self.ahat.free()

@@ -37,10 +37,12 @@ def test_spgemm_c_matches_scipy_order():
         assert_bitwise(osp.spgemm_c(a, b).m, (a @ b).tocsr())
 
 
+@pytest.mark.parametrize("post", [False, True])
 @pytest.mark.parametrize("cfg,edge", [(1, 16), (2, 6), (4, 5)])
-def test_reference_mgr_with_oracle_amg_seam(ncpflow, cfg, edge, monkeypatch):
+def test_reference_mgr_with_oracle_amg_seam(ncpflow, cfg, edge, post, monkeypatch):
     """The reference's own MGR + GMRES with the oracle AMG plugged into the
-    ``ncpflow.mgr.amg_mod`` seam reproduces the oracle pipeline exactly."""
+    ``ncpflow.mgr.amg_mod`` seam reproduces the oracle pipeline exactly, in both MGR
+    sweep orders (``post_smoothing``, mgr.py:362-368)."""
     import ncpflow.krylov as rkr
     import ncpflow.mgr as rmgr
     from ncpflow.sparse import CsrMatrix
@@ -53,11 +55,11 @@ def test_reference_mgr_with_oracle_amg_seam(ncpflow, cfg, edge, monkeypatch):
     plan = [(f, rmgr.MgrLevelSpec((), rp, rmgr.FRelax("amg", pre=1, post=1)))
             for f in synth.mgr_f_indices(s.b, s.n_cells)]
     opts = oamg.AmgOptions(pre_sweeps=2, post_sweeps=2)
-    h = rmgr.setup_from_matrix(CsrMatrix(ahat), plan, opts)
+    h = rmgr.setup_from_matrix(CsrMatrix(ahat), plan, opts, post_smoothing=post)
     rref = rkr.gmres(lambda v: a @ v, lambda v: rmgr.mgr_apply(h, obs.prescale(g, v)), s.rhs,
                      rkr.GmresOptions(rel_tol=1e-10))
     plan_o = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", pre=1, post=1))
-    ro, ho, _ = opipe.solve_synthetic(s, rel_tol=1e-10, plan=plan_o, amg_opts=opts)
+    ro, ho, _ = opipe.solve_synthetic(s, rel_tol=1e-10, plan=plan_o, amg_opts=opts, post_smoothing=post)
     assert ro.iterations == rref.iterations
     assert relerr(ro.x, rref.x) <= 1e-12
     for lr, lo in zip(h.levels, ho.levels):
@@ -196,7 +198,7 @@ def test_oracle_self_perturbation_moves_iterations():
     s = synth.make_config(3, 11)
     plan = opipe.default_plan(s.b, s.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX))
     opts = oamg.AmgOptions(**dict(gpipe.DEFAULT_AMG, coarse_size_cutoff=gpipe.REFERENCE_CUTOFF))
-    state, _ = opipe.setup_synthetic(s, amg_opts=opts, plan=plan)
+    state, _ = opipe.setup_synthetic(s, amg_opts=opts, plan=plan, post_smoothing=False)
     base = opipe.gmres_synthetic(state, s.rhs, rel_tol=1e-10)
     runs = [opipe.gmres_synthetic(state, s.rhs, rel_tol=1e-10, perturb_seed=100 + k, mode="noise") for k in range(1, 9)]
     its = [base.iterations] + [r.iterations for r in runs]
@@ -205,7 +207,7 @@ def test_oracle_self_perturbation_moves_iterations():
         assert r.converged and np.linalg.norm(r.x - base.x) <= 1e-8 * np.linalg.norm(base.x)
     s10 = synth.make_config(3, 10)
     state10, _ = opipe.setup_synthetic(s10, amg_opts=opts, plan=opipe.default_plan(
-        s10.b, s10.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX)))
+        s10.b, s10.n_cells, frelax=omgr.FRelax("amg", **gpipe.DEFAULT_FRELAX)), post_smoothing=False)
     st = {}
     r10 = opipe.gmres_synthetic(state10, s10.rhs, rel_tol=1e-10, stats=st)
     tol = 1e-10 * r10.rhs_norm

@@ -25,7 +25,7 @@ def run(ctx, s, label, kv, reps=3, warm=2):
     gr = False
     fr_kind, fr_sweeps = "amg", 1
     rp = None
-    post = False
+    post = None
     for k, v in kv.items():
         if k == "gr":
             gr = bool(int(v))
