@@ -124,3 +124,18 @@ def test_variable_major_layout_matches_cell_major():
     N, b = s.n_cells, s.b
     perm = (np.arange(s.n) % b) * N + np.arange(s.n) // b   # cell-major index -> var-major index
     np.testing.assert_array_equal(a_var[perm][:, perm].toarray(), a_cell.toarray())
+
+
+def test_pipeline_defaults_mirrored_in_the_oracle():
+    """The synthetic pipeline's DESIGN decisions are the same on both sides of every
+    parity test: MGR sweep order per block size and the default R/P kind."""
+    from oracle import pipeline as opipe
+    from paper_1801_08464_b200 import pipeline as gpipe
+    for b in (1, 2, 3):
+        assert gpipe.default_post_smoothing(b) == opipe.default_post_smoothing(b)
+    assert gpipe.default_post_smoothing(2) and not gpipe.default_post_smoothing(3)
+    for b, ncell in ((2, 8), (3, 8)):
+        pg = gpipe.default_plan(b, ncell)
+        po = opipe.default_plan(b, ncell)
+        assert [s.rp.value for _, s in pg] == [s.rp.value for _, s in po]
+        assert len(pg) == b - 1
