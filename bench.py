@@ -260,6 +260,17 @@ def _avail_gb():
     return 16.0
 
 
+def _mgr_desc(b):
+    """The solver options both arms run (pipeline defaults, mirrored in oracle/pipeline.py)."""
+    from paper_1801_08464_b200 import pipeline as gp
+    order = "coarse correction then F-relaxation (post_smoothing)" if gp.default_post_smoothing(b) \
+        else "F-relaxation then coarse correction"
+    kind = "NONINJECTIVE" if b == 2 else "INJECTIVE"
+    return (f"{b}-level MGR, R/P {kind}, {order}; F-relaxation AMG V(1,1), coarse AMG V(1,1), PMIS / extended+i "
+            f"(max_elmts {gp.DEFAULT_AMG['max_elmts']}) / L1-Jacobi, theta {gp.DEFAULT_AMG['strength_theta']}, "
+            f"coarse cutoff {gp.DEFAULT_AMG['coarse_size_cutoff']}; GMRES(30)")
+
+
 def reference_arm(args, ws, rank):
     """--impl reference: the reference's algorithm on the host cores -- the CPU oracle
     port (the reference is pure Python; oracle/pipeline.py restates its MGR + GMRES
@@ -296,7 +307,8 @@ def reference_arm(args, ws, rank):
             "data": "synthetic (seeded BASELINE config generator)", "impl": "reference",
             "config": {"workload": f"BASELINE config {args.config}: {edge_s} b={s.b}, {n} DOFs, "
                                    f"GMRES(30)+MGR rtol 1e-8",
-                       "dofs": n, "parallelism": f"{procs} concurrent single-threaded CPU processes, "
+                       "dofs": n, "mgr": _mgr_desc(s.b),
+                       "parallelism": f"{procs} concurrent single-threaded CPU processes, "
                                                  f"{nsolve} full solves (one wave; --steps {args.steps})"},
             "iterations": its[-1], "converged": all(r["converged"] for r in rs),
             "setup_s_median": statistics.median(r["setup_s"] for r in rs),
@@ -449,7 +461,8 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE config generator)",
                 "config": {"workload": f"BASELINE config {args.config}: {sysm.nx}x{sysm.ny}x{sysm.nz} b={sysm.b}, "
                                        f"{n} DOFs, GMRES(30)+MGR rtol 1e-8",
-                           "dofs": n, "nnzb": sysm.nnzb, "l2": "inputs larger than L2 (BCSR A ~600 MB at 128^3)",
+                           "dofs": n, "nnzb": sysm.nnzb, "mgr": _mgr_desc(sysm.b),
+                           "l2": "inputs larger than L2 (BCSR A ~600 MB at 128^3)",
                            "parallelism": f"replicas x{ws}"},
                 "iterations": its[-1], "converged": conv, "setup_ms": statistics.median(setup_ms),
                 "solve_ms": statistics.median(solve_ms),
